@@ -1,0 +1,170 @@
+/*
+ * sparsedrop_b200.h — the C-ABI drop-in boundary of the B200 SparseDrop path.
+ *
+ * Plain C: device pointers, sizes, a stream handle (cudaStream_t passed as
+ * void*). No torch or C++ types cross this boundary. Every entry point replaces
+ * one symbol of the reference's C++ operator API (namespace sparsedrop,
+ * /root/reference/proj/include/sparsedrop/), cited per function below; the C++
+ * wrapper include/sparsedrop_b200.hpp and the Python package
+ * paper_2411_01238_b200 restore the reference's names, ownership and exception
+ * types on top of it.
+ *
+ * Conventions
+ *  - All matrices are dense row-major (matrix.hpp:11, element (i,j) at
+ *    i*cols+j), bf16 (1) or fp32 (0) as tagged, 16-byte aligned.
+ *  - Calls are stream-ordered and asynchronous; nothing allocates on the hot
+ *    path. Buffers are caller-owned device memory.
+ *  - Status codes: SD_OK, or SD_EINVAL (the reference throws
+ *    std::invalid_argument), SD_ERANGE (std::out_of_range), SD_ERUNTIME
+ *    (std::runtime_error: CUDA errors, missing device). sd_last_error() returns
+ *    the message of the calling thread's last failure; messages keep the
+ *    reference substrings ("m_blk", "k_blk", "does not divide",
+ *    "gemm shape mismatch", "mask geometry").
+ *  - There is no CPU fallback: without a B200 (sm_100) device every compute
+ *    call returns SD_ERUNTIME.
+ */
+#ifndef SPARSEDROP_B200_H
+#define SPARSEDROP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SD_API __attribute__((visibility("default")))
+#else
+#define SD_API
+#endif
+
+#define SD_OK 0
+#define SD_EINVAL 1
+#define SD_ERANGE 2
+#define SD_ERUNTIME 3
+
+#define SD_DTYPE_F32 0
+#define SD_DTYPE_BF16 1
+
+#define SD_ABI_VERSION 1
+
+/* Device-resident block mask plus the compaction products the GEMMs consume.
+ * Mirrors sparsedrop::BlockMask (block_mask.hpp:31-76): grid block_rows x
+ * block_cols of m_blk x k_blk blocks, bit b = r*block_cols + c LSB-first in
+ * words[b/64], set = KEEP, padding bits zero. row_block_offset is the GLOBAL
+ * index of local block row 0 for a row shard (0 for an unsharded mask).
+ * Bind the pointers with sd_mask_bind() over one device workspace of
+ * sd_mask_workspace_bytes() bytes (zero-initialised once before first use). */
+typedef struct sd_block_mask {
+    int32_t block_rows, block_cols, m_blk, k_blk, row_block_offset, reserved;
+    uint64_t* words;      /* ceil(R*C/64) mask words                              */
+    int64_t* keep_count;  /* 1: popcount of the words                             */
+    int32_t* row_cnt;     /* R: kept blocks per block row                          */
+    int32_t* row_idx;     /* R*C: kept_blocks_in_row(mask, r), row stride C        */
+    int32_t* col_cnt;     /* C: kept blocks per block column                      */
+    int32_t* col_idx;     /* C*R: kept_blocks_in_row(transpose_mask(mask), c)     */
+    int32_t* row_order;   /* R: block rows by kept count, descending (scheduling)  */
+    int32_t* col_order;   /* C: block columns by kept count, descending           */
+    uint32_t* ticket;     /* 1: internal completion counter (keep zero)           */
+} sd_block_mask;
+
+SD_API int sd_abi_version(void);
+SD_API const char* sd_last_error(void);
+/* Number of usable sm_100 devices (0 when none: compute calls then fail). */
+SD_API int sd_device_count(void);
+
+/* Workspace size for a block_rows x block_cols mask and its compaction lists. */
+SD_API size_t sd_mask_workspace_bytes(int32_t block_rows, int32_t block_cols);
+/* Carve `workspace` into the mask's arrays and record the geometry
+ * (block_mask.hpp:31-41, BlockMask(block_rows, block_cols, m_blk, k_blk)). */
+SD_API int sd_mask_bind(sd_block_mask* mask, void* workspace, int32_t block_rows, int32_t block_cols,
+                 int32_t m_blk, int32_t k_blk, int32_t row_block_offset);
+
+/* Replaces sparsedrop::sample_mask(const DropoutSpec&, int rows, int cols)
+ * (block_mask.hpp:81, block_mask.cpp:52-80): validates p in [0,1) and that
+ * m_blk | rows, k_blk | cols against `mask`'s block extents, then draws one
+ * splitmix64 counter-hash bit per block, keep iff
+ * unit_interval(counter_hash(seed, row_block_offset + r, c)) >= p — bit-exact
+ * with the reference — and fills the compaction lists (kept_blocks_in_row on
+ * the mask and on transpose_mask(mask), block_mask.cpp:117-135) in the same
+ * launch. `rows` x `cols` are the LOCAL element extents of the mask. */
+SD_API int sd_mask_sample(sd_block_mask* mask, uint64_t seed, double p, int32_t rows, int32_t cols,
+                   void* stream);
+
+/* Replaces mask_from_words + the compaction: `mask->words` already holds the
+ * bits (e.g. uploaded from a host BlockMask); rebuild keep_count and lists.
+ * (block_mask.cpp:82-98 — padding validation is the host wrapper's job.) */
+SD_API int sd_mask_compact(sd_block_mask* mask, void* stream);
+
+/* Replaces sparsedrop::transpose_mask (block_mask.cpp:117-123): `out` must be
+ * bound with the swapped geometry (block_cols x block_rows, k_blk x m_blk). */
+SD_API int sd_mask_transpose(const sd_block_mask* in, sd_block_mask* out, void* stream);
+
+/* Replaces sparsedrop::retile (block_mask.cpp:100-115): `out` must be bound
+ * with grid (R*split_m) x (C*split_k) and blocks (m_blk/split_m) x (k_blk/split_k). */
+SD_API int sd_mask_retile(const sd_block_mask* in, int32_t split_m, int32_t split_k, sd_block_mask* out,
+                   void* stream);
+
+/* Replaces sparsedrop::dense_gemm (gemm.hpp:104-128): c = a * b,
+ * a: m x k bf16, b: k x n bf16, c: m x n (c_dtype). tcgen05 GEMM.
+ * Requires m % 128 == 0, n % 128 == 0, k % 64 == 0. */
+SD_API int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                  int32_t k, void* stream);
+
+/* Replaces sparsedrop::dsd_matmul (gemm.hpp:133-170):
+ * c = scale * (a (.) expand(mask)) * b — dropped K-blocks of `a` are never
+ * read. mask geometry must equal (m/m_blk) x (k/k_blk) blocks of m_blk x k_blk
+ * (gemm.hpp:139-140). kblock_per_tile_row (optional, m/128 u64 device
+ * counters, zeroed by the caller) accumulates executed 128x128x128 block
+ * products per 128-row tile row (KernelCounters, gemm.hpp:31-37, n_blk = 128). */
+SD_API int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
+                  int32_t c_dtype, int32_t m, int32_t n, int32_t k,
+                  unsigned long long* kblock_per_tile_row, void* stream);
+
+/* Replaces sparsedrop::sdd_matmul (gemm.hpp:176-213):
+ * c = scale * (a * b) restricted to kept OUTPUT blocks, a: m x k, b: k x n
+ * row-major; dropped output blocks are written as exact +0.0 (never computed).
+ * mask geometry must equal (m/m_blk) x (n/n_blk) with n_blk = mask->k_blk. */
+SD_API int sd_sdd_matmul(const void* a, const void* b, const sd_block_mask* mask, float scale, void* c,
+                  int32_t c_dtype, int32_t m, int32_t n, int32_t k,
+                  unsigned long long* kblock_per_tile_row, void* stream);
+
+/* Fused dropout+linear layer (layer.hpp:85-162), operands in place — no
+ * materialised transposes (the reference copies W^T and x^T, layer.hpp:158-160).
+ * x: m x k bf16, w: k x n bf16, dy: m x n bf16, mask over x (m/m_blk x k/k_blk).
+ *  forward:      y  = scale * (x (.) m) w                          (layer.hpp:115)
+ *  backward dX:  dx = scale * (dy w^T) (.) m   (sdd, W read K-major) (layer.hpp:158)
+ *  backward dW:  dw = scale * (x (.) m)^T dy   (dsd over column lists) (layer.hpp:159-160)
+ * scale = float(1.0/(1.0-p)) as dropout_scale<float> (layer.hpp:78-81). */
+SD_API int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
+                      int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream);
+SD_API int sd_linear_backward_dx(const void* dy, const void* w, const sd_block_mask* mask, float scale,
+                          void* dx, int32_t dx_dtype, int32_t m, int32_t n, int32_t k,
+                          void* stream);
+SD_API int sd_linear_backward_dw(const void* x, const sd_block_mask* mask, const void* dy, float scale,
+                          void* dw, int32_t dw_dtype, int32_t m, int32_t n, int32_t k,
+                          void* stream);
+
+/* Dense backward GEMMs for the dense fwd+bwd baseline (layer.hpp:140-145):
+ * dx = dy w^T (w read in place), dw = x^T dy (x read in place). */
+SD_API int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, int32_t m,
+                     int32_t n, int32_t k, void* stream); /* c[m,n] = a[m,k] * b_t[n,k]^T */
+SD_API int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, int32_t m,
+                     int32_t n, int32_t k, void* stream); /* c[m,n] = a_t[k,m]^T * b[k,n] */
+
+/* Effective FLOPs (gemm.hpp:217-228): kind 0 = dsd (2*n*m_blk*k_blk*keep),
+ * 1 = sdd (2*k*m_blk*n_blk*keep). */
+SD_API uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k);
+SD_API uint64_t sd_flops_effective(int64_t n, int64_t k, int32_t m_blk, int32_t n_blk, int32_t k_blk,
+                            int64_t keep, int32_t kind);
+
+/* Launch counter: number of kernels this library has enqueued (evidence that the
+ * native path ran; see bench.py "gpu_launches"). */
+SD_API uint64_t sd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSEDROP_B200_H */

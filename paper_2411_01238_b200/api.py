@@ -1,0 +1,445 @@
+"""Host-side mirror of the reference's C++ operator API on B200 device memory.
+
+Names, argument meaning and error behaviour follow namespace ``sparsedrop`` of
+the reference (/root/reference/proj/include/sparsedrop/): ``TileConfig``,
+``DropoutSpec``, ``BlockMask``, ``sample_mask``, ``kept_blocks_in_row``,
+``transpose_mask``, ``retile``, ``dense_gemm``, ``dsd_matmul``, ``sdd_matmul``,
+``LinearLayer``, ``forward``, ``backward``, ``flops_dense``, ``flops_effective``.
+Differences, all forced by the device:
+  * matrices are CUDA ``torch.Tensor`` s (bf16 inputs, row-major contiguous) —
+    torch is only the allocator / stream plumbing; every op is one call into
+    libsparsedrop_b200.so through the C-ABI;
+  * ``threads=`` is replaced by the current CUDA stream;
+  * exceptions: std::invalid_argument -> ValueError, std::out_of_range ->
+    IndexError, std::runtime_error -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import enum
+from typing import Optional
+
+import torch
+
+from . import _capi
+from ._capi import SD_DTYPE_BF16, SD_DTYPE_F32, SdBlockMask, check
+
+
+def _lib():
+    return _capi.load()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _dtype_code(dtype: torch.dtype) -> int:
+    if dtype == torch.bfloat16:
+        return SD_DTYPE_BF16
+    if dtype == torch.float32:
+        return SD_DTYPE_F32
+    raise ValueError(f"unsupported output dtype {dtype} (bf16 or fp32)")
+
+
+def _require_bf16(name: str, t: torch.Tensor) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
+    if t.dtype != torch.bfloat16 or t.dim() != 2 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous 2-D bf16 tensor, got {t.dtype} {tuple(t.shape)}")
+
+
+# --------------------------------------------------------------------------- rng.hpp
+
+MASK64 = (1 << 64) - 1
+
+
+def mix64(z: int) -> int:
+    """rng.hpp:11-16 (host helper for seeds; the device kernel hashes the blocks)."""
+    z = (z + 0x9E3779B97F4A7C15) & MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def counter_hash(seed: int, a: int, b: int) -> int:
+    """rng.hpp:18-20."""
+    return mix64(mix64(mix64(seed & MASK64) ^ (a & MASK64)) ^ (b & MASK64))
+
+
+def effective_seed(spec_seed: int, step_seed: int, layer_index: int) -> int:
+    """layer.hpp:64-67: one seed per (layer instance, step)."""
+    return counter_hash(spec_seed, step_seed, layer_index & MASK64)
+
+
+def dropout_scale(p: float) -> float:
+    """layer.hpp:78-81 dropout_scale<float>: float(1.0 / (1.0 - p))."""
+    import numpy as np
+
+    return float(np.float32(1.0 / (1.0 - p)))
+
+
+# --------------------------------------------------------------------------- block_mask.hpp
+
+
+@dataclasses.dataclass
+class TileConfig:
+    """block_mask.hpp:14-18. On B200 the kernel tile is fixed (128 x 256 x 64);
+    TileConfig here only carries the mask block sizes used for validation."""
+
+    m_blk: int = 128
+    n_blk: int = 128
+    k_blk: int = 128
+
+
+@dataclasses.dataclass
+class DropoutSpec:
+    """block_mask.hpp:21-26."""
+
+    p: float = 0.0
+    m_blk: int = 128
+    k_blk: int = 128
+    seed: int = 0
+
+
+class BlockMask:
+    """Device-resident sparsedrop::BlockMask (block_mask.hpp:31-76) plus the
+    compaction lists the GEMMs consume (row lists = kept_blocks_in_row, column
+    lists = kept_blocks_in_row of transpose_mask)."""
+
+    def __init__(self, block_rows: int, block_cols: int, m_blk: int, k_blk: int,
+                 row_block_offset: int = 0, device=None):
+        if block_rows <= 0 or block_cols <= 0 or m_blk <= 0 or k_blk <= 0:
+            raise ValueError(
+                f"BlockMask geometry must be positive: grid {block_rows}x{block_cols}, "
+                f"blocks {m_blk}x{k_blk}")
+        lib = _lib()
+        nbytes = lib.sd_mask_workspace_bytes(block_rows, block_cols)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # zero-initialised once: all-clear mask, re-armed completion ticket
+        self._ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=dev)
+        base = self._ws.data_ptr()
+        aligned = (base + 255) & ~255
+        self._c = SdBlockMask()
+        check(lib.sd_mask_bind(ctypes.byref(self._c), ctypes.c_void_p(aligned), block_rows, block_cols,
+                               m_blk, k_blk, row_block_offset))
+        self._base_off = aligned - base
+        self.device = self._ws.device
+
+    # geometry (block_mask.hpp:41-52)
+    def block_rows(self) -> int: return self._c.block_rows
+    def block_cols(self) -> int: return self._c.block_cols
+    def m_blk(self) -> int: return self._c.m_blk
+    def k_blk(self) -> int: return self._c.k_blk
+    def rows(self) -> int: return self._c.block_rows * self._c.m_blk
+    def cols(self) -> int: return self._c.block_cols * self._c.k_blk
+    def row_block_offset(self) -> int: return self._c.row_block_offset
+    def total_blocks(self) -> int: return self._c.block_rows * self._c.block_cols
+    def n_words(self) -> int: return (self.total_blocks() + 63) // 64
+
+    def _view(self, field: str, count: int, dtype: torch.dtype) -> torch.Tensor:
+        off = getattr(self._c, field) - self._ws.data_ptr()
+        nbytes = count * torch.tensor([], dtype=dtype).element_size()
+        return self._ws[off:off + nbytes].view(dtype)
+
+    # device views (no copies)
+    def words_device(self) -> torch.Tensor: return self._view("words", self.n_words(), torch.int64)
+    def keep_count_device(self) -> torch.Tensor: return self._view("keep_count", 1, torch.int64)
+    def row_cnt_device(self) -> torch.Tensor: return self._view("row_cnt", self.block_rows(), torch.int32)
+    def row_idx_device(self) -> torch.Tensor:
+        return self._view("row_idx", self.total_blocks(), torch.int32).view(self.block_rows(), self.block_cols())
+    def col_cnt_device(self) -> torch.Tensor: return self._view("col_cnt", self.block_cols(), torch.int32)
+    def col_idx_device(self) -> torch.Tensor:
+        return self._view("col_idx", self.total_blocks(), torch.int32).view(self.block_cols(), self.block_rows())
+    def row_order_device(self) -> torch.Tensor: return self._view("row_order", self.block_rows(), torch.int32)
+    def col_order_device(self) -> torch.Tensor: return self._view("col_order", self.block_cols(), torch.int32)
+
+    # host reads (block_mask.hpp:46-62)
+    def words(self) -> list:
+        return [w & MASK64 for w in self.words_device().cpu().tolist()]
+
+    def keep_count(self) -> int:
+        return int(self.keep_count_device().item())
+
+    def realized_sparsity(self) -> float:
+        t = self.total_blocks()
+        return 0.0 if t == 0 else 1.0 - self.keep_count() / t
+
+    def kept(self, block_row: int, block_col: int) -> bool:
+        b = block_row * self.block_cols() + block_col
+        w = int(self.words_device()[b >> 6].item()) & MASK64
+        return bool((w >> (b & 63)) & 1)
+
+    @property
+    def c_struct(self) -> SdBlockMask:
+        return self._c
+
+    def cptr(self):
+        return ctypes.byref(self._c)
+
+
+def sample_mask(spec: DropoutSpec, rows: int, cols: int, row_block_offset: int = 0,
+                stream=None, out: Optional[BlockMask] = None) -> BlockMask:
+    """block_mask.cpp:52-80 on the device (bit-exact splitmix64 draw), plus the
+    compaction lists. `row_block_offset` selects the global block rows of a
+    row shard. Raises ValueError like the reference's invalid_argument."""
+    if not (0.0 <= spec.p < 1.0):
+        raise ValueError(f"dropout rate must lie in [0, 1), got {spec.p:f}")
+    if spec.m_blk <= 0 or rows % spec.m_blk != 0:
+        raise ValueError(f"mask block size m_blk={spec.m_blk} does not divide rows={rows}")
+    if spec.k_blk <= 0 or cols % spec.k_blk != 0:
+        raise ValueError(f"mask block size k_blk={spec.k_blk} does not divide cols={cols}")
+    m = out if out is not None else BlockMask(rows // spec.m_blk, cols // spec.k_blk, spec.m_blk,
+                                              spec.k_blk, row_block_offset)
+    check(_lib().sd_mask_sample(m.cptr(), spec.seed & MASK64, float(spec.p), rows, cols,
+                                ctypes.c_void_p(_stream(stream))))
+    return m
+
+
+def mask_from_words(block_rows: int, block_cols: int, m_blk: int, k_blk: int, words,
+                    stream=None) -> BlockMask:
+    """block_mask.cpp:82-98: validates word count and zero padding, uploads, compacts."""
+    words = [int(w) & MASK64 for w in words]
+    bits = block_rows * block_cols
+    if len(words) != (bits + 63) // 64:
+        raise ValueError(f"BlockMask word count {len(words)} does not match grid of {bits} bits")
+    if bits & 63 and words[-1] & (MASK64 ^ ((1 << (bits & 63)) - 1)):
+        raise ValueError("BlockMask has nonzero bits past the block grid")
+    m = BlockMask(block_rows, block_cols, m_blk, k_blk)
+    signed = [w - (1 << 64) if w >= (1 << 63) else w for w in words]
+    m.words_device().copy_(torch.tensor(signed, dtype=torch.int64))
+    check(_lib().sd_mask_compact(m.cptr(), ctypes.c_void_p(_stream(stream))))
+    return m
+
+
+def transpose_mask(mask: BlockMask, stream=None) -> BlockMask:
+    """block_mask.cpp:117-123."""
+    out = BlockMask(mask.block_cols(), mask.block_rows(), mask.k_blk(), mask.m_blk())
+    check(_lib().sd_mask_transpose(mask.cptr(), out.cptr(), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def retile(mask: BlockMask, split_m: int, split_k: int, stream=None) -> BlockMask:
+    """block_mask.cpp:100-115."""
+    if split_m <= 0 or mask.m_blk() % split_m != 0:
+        raise ValueError(f"split_m={split_m} does not divide m_blk={mask.m_blk()}")
+    if split_k <= 0 or mask.k_blk() % split_k != 0:
+        raise ValueError(f"split_k={split_k} does not divide k_blk={mask.k_blk()}")
+    out = BlockMask(mask.block_rows() * split_m, mask.block_cols() * split_k,
+                    mask.m_blk() // split_m, mask.k_blk() // split_k)
+    check(_lib().sd_mask_retile(mask.cptr(), split_m, split_k, out.cptr(), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def kept_blocks_in_row(mask: BlockMask, block_row: int) -> list:
+    """block_mask.cpp:125-135, read from the device row lists."""
+    if block_row < 0 or block_row >= mask.block_rows():
+        raise IndexError(f"block row {block_row} outside grid with {mask.block_rows()} rows")
+    n = int(mask.row_cnt_device()[block_row].item())
+    return mask.row_idx_device()[block_row, :n].cpu().tolist()
+
+
+# --------------------------------------------------------------------------- gemm.hpp
+
+@dataclasses.dataclass
+class KernelCounters:
+    """gemm.hpp:31-37: executed 128x128x128 block products per 128-row tile row."""
+
+    kblock_iterations: int = 0
+    kblock_per_tile_row: list = dataclasses.field(default_factory=list)
+
+
+def _out(m: int, n: int, dtype: torch.dtype, device) -> torch.Tensor:
+    return torch.empty(m, n, dtype=dtype, device=device)
+
+
+def dense_gemm(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.bfloat16, stream=None,
+               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm.hpp:104-128: c = a * b on the tcgen05 tensor cores."""
+    _require_bf16("a", a), _require_bf16("b", b)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"gemm shape mismatch: {a.shape[0]}x{a.shape[1]} * {b.shape[0]}x{b.shape[1]}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = out if out is not None else _out(m, n, out_dtype, a.device)
+    check(_lib().sd_dense_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), _dtype_code(c.dtype), m, n, k,
+                               ctypes.c_void_p(_stream(stream))))
+    return c
+
+
+def _counters_buf(rows: int, device, counters: Optional[KernelCounters]):
+    if counters is None:
+        return None
+    return torch.zeros(rows // 128, dtype=torch.int64, device=device)
+
+
+def _fill_counters(counters: Optional[KernelCounters], buf: Optional[torch.Tensor]) -> None:
+    if counters is None:
+        return
+    per = buf.cpu().tolist()
+    counters.kblock_per_tile_row = per
+    counters.kblock_iterations = sum(per)
+
+
+def dsd_matmul(a: torch.Tensor, mask: BlockMask, b: torch.Tensor, scale_factor: float,
+               tiles: Optional[TileConfig] = None, counters: Optional[KernelCounters] = None,
+               out_dtype=torch.bfloat16, stream=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm.hpp:133-170: scale * (a (.) expand(mask)) * b; dropped K-blocks never read."""
+    _require_bf16("a", a), _require_bf16("b", b)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"gemm shape mismatch: {a.shape[0]}x{a.shape[1]} * {b.shape[0]}x{b.shape[1]}")
+    if tiles is not None and (tiles.m_blk != mask.m_blk() or tiles.k_blk != mask.k_blk()):
+        raise ValueError("dsd_matmul: mask geometry does not match problem (tile sizes)")
+    m, k = a.shape
+    n = b.shape[1]
+    c = out if out is not None else _out(m, n, out_dtype, a.device)
+    cb = _counters_buf(m, a.device, counters)
+    check(_lib().sd_dsd_matmul(a.data_ptr(), mask.cptr(), b.data_ptr(), float(scale_factor), c.data_ptr(),
+                               _dtype_code(c.dtype), m, n, k, _ptr(cb), ctypes.c_void_p(_stream(stream))))
+    _fill_counters(counters, cb)
+    return c
+
+
+def sdd_matmul(a: torch.Tensor, b: torch.Tensor, mask: BlockMask, scale_factor: float,
+               tiles: Optional[TileConfig] = None, counters: Optional[KernelCounters] = None,
+               out_dtype=torch.bfloat16, stream=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm.hpp:176-213: scale * (a * b) on kept OUTPUT blocks, exact +0.0 elsewhere."""
+    _require_bf16("a", a), _require_bf16("b", b)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"gemm shape mismatch: {a.shape[0]}x{a.shape[1]} * {b.shape[0]}x{b.shape[1]}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = out if out is not None else _out(m, n, out_dtype, a.device)
+    cb = _counters_buf(m, a.device, counters)
+    check(_lib().sd_sdd_matmul(a.data_ptr(), b.data_ptr(), mask.cptr(), float(scale_factor), c.data_ptr(),
+                               _dtype_code(c.dtype), m, n, k, _ptr(cb), ctypes.c_void_p(_stream(stream))))
+    _fill_counters(counters, cb)
+    return c
+
+
+class SparseKind(enum.Enum):
+    dsd = 0
+    sdd = 1
+
+
+def flops_dense(m: int, n: int, k: int) -> int:
+    """gemm.hpp:217-219."""
+    return 2 * m * n * k
+
+
+def flops_effective(m: int, n: int, k: int, tiles: TileConfig, mask: BlockMask, kind: SparseKind) -> int:
+    """gemm.hpp:222-228."""
+    keep = mask.keep_count()
+    if kind == SparseKind.dsd:
+        return 2 * n * tiles.m_blk * tiles.k_blk * keep
+    return 2 * k * tiles.m_blk * tiles.n_blk * keep
+
+
+# --------------------------------------------------------------------------- layer.hpp
+
+class LinearVariant(enum.Enum):
+    dense = 0
+    dropout_dense = 1
+    sparsedrop = 2
+
+
+@dataclasses.dataclass
+class LinearLayer:
+    """layer.hpp:29-47. weight is K x N bf16 on the device."""
+
+    kind: LinearVariant
+    weight: torch.Tensor
+    spec: DropoutSpec
+    tiles: TileConfig = dataclasses.field(default_factory=TileConfig)
+    layer_index: int = 0
+
+    def __post_init__(self):
+        if self.kind == LinearVariant.dropout_dense:
+            raise ValueError("dropout_dense is not implemented on the B200 path (out of scope, SURVEY §8f2)")
+        if self.kind == LinearVariant.sparsedrop and (
+                self.spec.m_blk != self.tiles.m_blk or self.spec.k_blk != self.tiles.k_blk):
+            raise ValueError("sparsedrop mask block sizes must equal the GEMM tile sizes")
+
+
+@dataclasses.dataclass
+class LayerContext:
+    """layer.hpp:51-58 (the input is referenced, not copied)."""
+
+    input: torch.Tensor
+    block_mask: Optional[BlockMask] = None
+    training: bool = False
+    step_seed: int = 0
+
+
+@dataclasses.dataclass
+class LayerGrads:
+    dx: torch.Tensor
+    dw: torch.Tensor
+
+
+def forward(layer: LinearLayer, x: torch.Tensor, train: bool, step_seed: int, stream=None,
+            out_dtype=torch.bfloat16, mask_out: Optional[BlockMask] = None):
+    """layer.hpp:85-117: returns (y, ctx). Training + sparsedrop samples one block
+    mask per (layer, step) and runs the dsd forward; otherwise dense."""
+    _require_bf16("x", x)
+    if x.shape[1] != layer.weight.shape[0]:
+        raise ValueError(f"layer forward: input {x.shape[0]}x{x.shape[1]} does not match weight "
+                         f"{layer.weight.shape[0]}x{layer.weight.shape[1]}")
+    ctx = LayerContext(input=x, training=train, step_seed=step_seed)
+    if not train or layer.kind == LinearVariant.dense:
+        return dense_gemm(x, layer.weight, out_dtype=out_dtype, stream=stream), ctx
+    seed = effective_seed(layer.spec.seed, step_seed, layer.layer_index)
+    s = dropout_scale(layer.spec.p)
+    spec = dataclasses.replace(layer.spec, seed=seed)
+    ctx.block_mask = sample_mask(spec, x.shape[0], x.shape[1], stream=stream, out=mask_out)
+    m, k = x.shape
+    n = layer.weight.shape[1]
+    y = torch.empty(m, n, dtype=out_dtype, device=x.device)
+    check(_lib().sd_linear_forward(x.data_ptr(), ctx.block_mask.cptr(), layer.weight.data_ptr(), s, y.data_ptr(),
+                                   _dtype_code(out_dtype), m, n, k, ctypes.c_void_p(_stream(stream))))
+    return y, ctx
+
+
+def backward(layer: LinearLayer, ctx: LayerContext, dy: torch.Tensor, stream=None,
+             dx_dtype=torch.bfloat16, dw_dtype=torch.float32) -> LayerGrads:
+    """layer.hpp:128-162: dx = s (dy W^T) (.) m (sdd), dw = s (x (.) m)^T dy (dsd on
+    column lists) — W and x are read in place, no transposes are materialised.
+    dW is computed first so a data-parallel caller can start its allreduce while
+    dX runs."""
+    _require_bf16("dy", dy)
+    x = ctx.input
+    if dy.shape[0] != x.shape[0] or dy.shape[1] != layer.weight.shape[1]:
+        raise ValueError(f"layer backward: dy {dy.shape[0]}x{dy.shape[1]} does not match forward shapes "
+                         f"{x.shape[0]}x{x.shape[1]} * {layer.weight.shape[0]}x{layer.weight.shape[1]}")
+    m, k = x.shape
+    n = dy.shape[1]
+    st = ctypes.c_void_p(_stream(stream))
+    dx = torch.empty(m, k, dtype=dx_dtype, device=dy.device)
+    dw = torch.empty(k, n, dtype=dw_dtype, device=dy.device)
+    if not ctx.training or layer.kind == LinearVariant.dense or ctx.block_mask is None:
+        check(_lib().sd_dense_gemm_tn(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), _dtype_code(dw_dtype),
+                                      k, n, m, st))
+        check(_lib().sd_dense_gemm_nt(dy.data_ptr(), layer.weight.data_ptr(), dx.data_ptr(),
+                                      _dtype_code(dx_dtype), m, k, n, st))
+        return LayerGrads(dx, dw)
+    s = dropout_scale(layer.spec.p)
+    mask = ctx.block_mask
+    check(_lib().sd_linear_backward_dw(x.data_ptr(), mask.cptr(), dy.data_ptr(), s, dw.data_ptr(),
+                                       _dtype_code(dw_dtype), m, n, k, st))
+    check(_lib().sd_linear_backward_dx(dy.data_ptr(), layer.weight.data_ptr(), mask.cptr(), s, dx.data_ptr(),
+                                       _dtype_code(dx_dtype), m, n, k, st))
+    return LayerGrads(dx, dw)
+
+
+def launch_count() -> int:
+    """Kernels enqueued by libsparsedrop_b200.so in this process."""
+    return int(_lib().sd_launch_count())
+
+
+def device_count() -> int:
+    return int(_lib().sd_device_count())

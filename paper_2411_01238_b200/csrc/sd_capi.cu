@@ -1,0 +1,488 @@
+// sd_capi.cu — the extern "C" boundary (include/sparsedrop_b200.h).
+//
+// Validation mirrors the reference's exceptions and messages:
+//   sample_mask            block_mask.cpp:53-61
+//   check_gemm_shapes      gemm.hpp:62-70 (check_divides :55-60)
+//   check_mask_geometry    gemm.hpp:72-82
+// plus the B200 kernels' own geometry limits (128-row output tiles, 64-element
+// reduction stages, 128/256-wide mask blocks along the skipped dimension).
+// Errors never cross the boundary as exceptions: sd::Error -> status code +
+// thread-local message (sd_last_error).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "sd_internal.h"
+
+namespace sd {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return SD_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SD_ERUNTIME;
+    }
+}
+
+std::string str(long long v) { return std::to_string(v); }
+
+void require_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        fail(SD_ERUNTIME, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) fail(SD_ERUNTIME, "device is not sm_100 (B200); this library targets sm_100a only");
+}
+
+// gemm.hpp:55-60
+void check_divides(int block, int extent, const char* which) {
+    if (block <= 0 || extent % block != 0)
+        fail(SD_EINVAL, std::string("tile size ") + which + "=" + str(block) +
+                            " does not divide dimension " + str(extent));
+}
+
+// gemm.hpp:62-70 for c = a(m x k) * b(k x n), with the B200 tile limits.
+void check_gemm(int m, int n, int k) {
+    if (m <= 0 || n <= 0 || k <= 0)
+        fail(SD_EINVAL, "gemm shape mismatch: dimensions must be positive, got m=" + str(m) +
+                            " n=" + str(n) + " k=" + str(k));
+    check_divides(128, m, "m_blk");
+    check_divides(128, n, "n_blk");
+    check_divides(64, k, "k_blk");
+}
+
+// gemm.hpp:72-82
+void check_mask_geometry(const sd_block_mask* mask, int grid_rows, int grid_cols, int blk_rows,
+                         int blk_cols, const char* where) {
+    if (!mask) fail(SD_EINVAL, std::string(where) + ": null mask");
+    if (mask->block_rows != grid_rows || mask->block_cols != grid_cols || mask->m_blk != blk_rows ||
+        mask->k_blk != blk_cols)
+        fail(SD_EINVAL, std::string(where) + ": mask geometry (" + str(mask->block_rows) + "x" +
+                            str(mask->block_cols) + " blocks of " + str(mask->m_blk) + "x" +
+                            str(mask->k_blk) + ") does not match problem (" + str(grid_rows) + "x" +
+                            str(grid_cols) + " blocks of " + str(blk_rows) + "x" + str(blk_cols) +
+                            ")");
+}
+
+void check_ptr(const void* p, const char* name) {
+    if (!p) fail(SD_EINVAL, std::string("null pointer: ") + name);
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+        fail(SD_EINVAL, std::string(name) + " must be 16-byte aligned");
+}
+
+void check_dtype(int dt) {
+    if (dt != SD_DTYPE_F32 && dt != SD_DTYPE_BF16) fail(SD_EINVAL, "unknown output dtype " + str(dt));
+}
+
+// Mask-block limits of the tcgen05 kernels: the mask block along the OUTPUT
+// rows must cover whole 128-row tiles; along the reduction it must cover whole
+// 64-element stages; along sdd output columns it must be 128 or 256.
+void check_row_blk(int blk, const char* which) {
+    if (blk <= 0 || blk % 128 != 0)
+        fail(SD_EINVAL, std::string("mask block size ") + which + "=" + str(blk) +
+                            " unsupported on B200: must be a multiple of 128");
+}
+void check_red_blk(int blk, const char* which) {
+    if (blk <= 0 || blk % 64 != 0)
+        fail(SD_EINVAL, std::string("mask block size ") + which + "=" + str(blk) +
+                            " unsupported on B200: must be a multiple of 64");
+}
+void check_col_blk(int blk, const char* which) {
+    if (blk != 128 && blk != 256)
+        fail(SD_EINVAL, std::string("mask block size ") + which + "=" + str(blk) +
+                            " unsupported on B200: must be 128 or 256");
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+GemmArgs base_args(int rows_out, int cols_out, int red, float scale, void* out) {
+    GemmArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.rows_out = rows_out;
+    a.cols_out = cols_out;
+    a.red = red;
+    a.n_row_tiles = rows_out / kBM;
+    a.n_col_units = (cols_out + kBN - 1) / kBN;
+    a.red_blk = kBK;
+    a.out_row_blk = kBM;
+    a.out_col_blk = 128;
+    a.scale = scale;
+    a.out = out;
+    return a;
+}
+
+// Output tensor map: store box = 32 rows x 128 bytes.
+CUtensorMap out_map(void* c, int dt, int rows, int cols) {
+    const bool f32 = dt == SD_DTYPE_F32;
+    return make_tmap_2d(c, f32, cols, rows, f32 ? 32 : 64, 32);
+}
+
+// bf16 operand maps. K-major (reduction contiguous): box 64 x 128 rows.
+// MN-major (output dimension contiguous): box 64 x 64 reduction rows.
+CUtensorMap kmajor_map(const void* p, int red, int rows) { return make_tmap_2d(p, false, red, rows, 64, 128); }
+CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_2d(p, false, mn, red, 64, 64); }
+
+}  // namespace
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SD_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+    int n = 0;
+    check_cuda(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    if (dev >= 0 && dev < 64) cached[dev] = n;
+    return n;
+}
+
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                         uint32_t box_outer) {
+    std::call_once(g_encode_once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+        else
+            cudaGetLastError();
+    });
+    if (!g_encode) fail(SD_ERUNTIME, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = g_encode(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                2, const_cast<void*>(base), dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(SD_ERUNTIME, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
+                              ") for a " + std::to_string(outer) + "x" + std::to_string(inner) + " tensor");
+    return map;
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+int sd_abi_version(void) { return SD_ABI_VERSION; }
+
+const char* sd_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t sd_launch_count(void) { return g_launches.load(); }
+
+int sd_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int ok = 0;
+    for (int d = 0; d < n; ++d) {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10)
+            ++ok;
+    }
+    return ok;
+}
+
+// Layout of the mask workspace (each array 256-byte aligned):
+// words | keep_count | ticket | row_cnt | row_idx | col_cnt | col_idx | row_order | col_order
+static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+size_t sd_mask_workspace_bytes(int32_t R, int32_t C) {
+    if (R <= 0 || C <= 0) return 0;
+    const size_t rc = static_cast<size_t>(R) * C;
+    const size_t nwords = (rc + 63) / 64;
+    return align256(nwords * 8) + align256(8) + align256(4) + align256(4 * R) + align256(4 * rc) +
+           align256(4 * C) + align256(4 * rc) + align256(4 * R) + align256(4 * C);
+}
+
+int sd_mask_bind(sd_block_mask* m, void* ws, int32_t R, int32_t C, int32_t m_blk, int32_t k_blk,
+                 int32_t row_block_offset) {
+    return guarded([&] {
+        if (!m || !ws) fail(SD_EINVAL, "sd_mask_bind: null mask or workspace");
+        if (R <= 0 || C <= 0 || m_blk <= 0 || k_blk <= 0)
+            fail(SD_EINVAL, "BlockMask geometry must be positive: grid " + str(R) + "x" + str(C) +
+                                ", blocks " + str(m_blk) + "x" + str(k_blk));
+        if (row_block_offset < 0) fail(SD_EINVAL, "row_block_offset must be non-negative");
+        if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) fail(SD_EINVAL, "mask workspace must be 256-byte aligned");
+        const size_t rc = static_cast<size_t>(R) * C;
+        char* p = static_cast<char*>(ws);
+        m->block_rows = R;
+        m->block_cols = C;
+        m->m_blk = m_blk;
+        m->k_blk = k_blk;
+        m->row_block_offset = row_block_offset;
+        m->reserved = 0;
+        m->words = reinterpret_cast<uint64_t*>(p);
+        p += align256((rc + 63) / 64 * 8);
+        m->keep_count = reinterpret_cast<int64_t*>(p);
+        p += align256(8);
+        m->ticket = reinterpret_cast<uint32_t*>(p);
+        p += align256(4);
+        m->row_cnt = reinterpret_cast<int32_t*>(p);
+        p += align256(4 * static_cast<size_t>(R));
+        m->row_idx = reinterpret_cast<int32_t*>(p);
+        p += align256(4 * rc);
+        m->col_cnt = reinterpret_cast<int32_t*>(p);
+        p += align256(4 * static_cast<size_t>(C));
+        m->col_idx = reinterpret_cast<int32_t*>(p);
+        p += align256(4 * rc);
+        m->row_order = reinterpret_cast<int32_t*>(p);
+        p += align256(4 * static_cast<size_t>(R));
+        m->col_order = reinterpret_cast<int32_t*>(p);
+    });
+}
+
+// block_mask.cpp:52-80
+int sd_mask_sample(sd_block_mask* m, uint64_t seed, double p, int32_t rows, int32_t cols, void* stream) {
+    return guarded([&] {
+        if (!m) fail(SD_EINVAL, "sd_mask_sample: null mask");
+        if (!(p >= 0.0 && p < 1.0)) {
+            char buf[64];
+            std::snprintf(buf, sizeof buf, "%f", p);
+            fail(SD_EINVAL, std::string("dropout rate must lie in [0, 1), got ") + buf);
+        }
+        if (m->m_blk <= 0 || rows % m->m_blk != 0)
+            fail(SD_EINVAL, "mask block size m_blk=" + str(m->m_blk) + " does not divide rows=" + str(rows));
+        if (m->k_blk <= 0 || cols % m->k_blk != 0)
+            fail(SD_EINVAL, "mask block size k_blk=" + str(m->k_blk) + " does not divide cols=" + str(cols));
+        if (rows / m->m_blk != m->block_rows || cols / m->k_blk != m->block_cols)
+            fail(SD_EINVAL, "sd_mask_sample: mask geometry (" + str(m->block_rows) + "x" + str(m->block_cols) +
+                                " blocks) does not match rows=" + str(rows) + " cols=" + str(cols));
+        require_device();
+        // keep iff (h >> 11) * 2^-53 >= p  <=>  (h >> 11) >= ceil(p * 2^53)  (exact: p*2^53 is exact)
+        const uint64_t threshold = static_cast<uint64_t>(std::ceil(std::ldexp(p, 53)));
+        uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        launch_mask_plan(*m, false, z, threshold, as_stream(stream));
+    });
+}
+
+int sd_mask_compact(sd_block_mask* m, void* stream) {
+    return guarded([&] {
+        if (!m || !m->words) fail(SD_EINVAL, "sd_mask_compact: unbound mask");
+        require_device();
+        launch_mask_plan(*m, true, 0, 0, as_stream(stream));
+    });
+}
+
+int sd_mask_transpose(const sd_block_mask* in, sd_block_mask* out, void* stream) {
+    return guarded([&] {
+        if (!in || !out) fail(SD_EINVAL, "sd_mask_transpose: null mask");
+        if (out->block_rows != in->block_cols || out->block_cols != in->block_rows ||
+            out->m_blk != in->k_blk || out->k_blk != in->m_blk)
+            fail(SD_EINVAL, "sd_mask_transpose: output mask must have the swapped geometry");
+        require_device();
+        launch_mask_transpose(*in, *out, as_stream(stream));
+    });
+}
+
+int sd_mask_retile(const sd_block_mask* in, int32_t split_m, int32_t split_k, sd_block_mask* out,
+                   void* stream) {
+    return guarded([&] {
+        if (!in || !out) fail(SD_EINVAL, "sd_mask_retile: null mask");
+        if (split_m <= 0 || in->m_blk % split_m != 0)
+            fail(SD_EINVAL, "split_m=" + str(split_m) + " does not divide m_blk=" + str(in->m_blk));
+        if (split_k <= 0 || in->k_blk % split_k != 0)
+            fail(SD_EINVAL, "split_k=" + str(split_k) + " does not divide k_blk=" + str(in->k_blk));
+        if (out->block_rows != in->block_rows * split_m || out->block_cols != in->block_cols * split_k ||
+            out->m_blk != in->m_blk / split_m || out->k_blk != in->k_blk / split_k)
+            fail(SD_EINVAL, "sd_mask_retile: output mask geometry does not match the split");
+        require_device();
+        launch_mask_retile(*in, split_m, split_k, *out, as_stream(stream));
+    });
+}
+
+// ---------------------------------------------------------------- GEMMs
+
+int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                  int32_t k, void* stream) {
+    return guarded([&] {
+        check_gemm(m, n, k);
+        check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
+        require_device();
+        GemmArgs g = base_args(m, n, k, 1.0f, c);
+        launch_gemm(false, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
+                    mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
+    });
+}
+
+int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                     int32_t k, void* stream) {
+    return guarded([&] {
+        check_gemm(m, n, k);
+        check_ptr(a, "a"), check_ptr(b_t, "b_t"), check_ptr(c, "c"), check_dtype(c_dtype);
+        require_device();
+        GemmArgs g = base_args(m, n, k, 1.0f, c);
+        launch_gemm(false, false, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
+                    kmajor_map(b_t, k, n), out_map(c, c_dtype, m, n), g, as_stream(stream));
+    });
+}
+
+int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                     int32_t k, void* stream) {
+    return guarded([&] {
+        check_gemm(m, n, k);
+        check_ptr(a_t, "a_t"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
+        require_device();
+        GemmArgs g = base_args(m, n, k, 1.0f, c);
+        launch_gemm(true, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, mnmajor_map(a_t, m, k),
+                    mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
+    });
+}
+
+// gemm.hpp:133-170 / layer.hpp:115
+static void dsd_forward(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
+                        int c_dtype, int m, int n, int k, unsigned long long* counters, void* stream,
+                        const char* where) {
+    check_gemm(m, n, k);
+    check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
+    if (!mask) fail(SD_EINVAL, std::string(where) + ": null mask");
+    check_divides(mask->m_blk, m, "m_blk");
+    check_divides(mask->k_blk, k, "k_blk");
+    check_mask_geometry(mask, m / mask->m_blk, k / mask->k_blk, mask->m_blk, mask->k_blk, where);
+    check_row_blk(mask->m_blk, "m_blk");
+    check_red_blk(mask->k_blk, "k_blk");
+    require_device();
+    GemmArgs g = base_args(m, n, k, scale, c);
+    g.list_cnt = mask->row_cnt;
+    g.list_idx = mask->row_idx;
+    g.list_stride = mask->block_cols;
+    g.red_blk = mask->k_blk;
+    g.out_row_blk = mask->m_blk;
+    g.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
+    g.counters = counters;
+    launch_gemm(false, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
+                mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
+}
+
+int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
+                  int32_t c_dtype, int32_t m, int32_t n, int32_t k, unsigned long long* counters,
+                  void* stream) {
+    return guarded([&] { dsd_forward(a, mask, b, scale, c, c_dtype, m, n, k, counters, stream, "dsd_matmul"); });
+}
+
+int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
+                      int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
+    return guarded(
+        [&] { dsd_forward(x, mask, w, scale, y, y_dtype, m, n, k, nullptr, stream, "layer forward"); });
+}
+
+// gemm.hpp:176-213. b_kmajor: b is given as b^T (n x k row-major), i.e. the layer's W.
+static void sdd(const void* a, const void* b, bool b_kmajor, const sd_block_mask* mask, float scale,
+                void* c, int c_dtype, int m, int n, int k, unsigned long long* counters, void* stream,
+                const char* where) {
+    check_gemm(m, n, k);
+    check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
+    if (!mask) fail(SD_EINVAL, std::string(where) + ": null mask");
+    check_divides(mask->m_blk, m, "m_blk");
+    check_divides(mask->k_blk, n, "n_blk");
+    check_mask_geometry(mask, m / mask->m_blk, n / mask->k_blk, mask->m_blk, mask->k_blk, where);
+    check_row_blk(mask->m_blk, "m_blk");
+    check_col_blk(mask->k_blk, "n_blk");
+    require_device();
+    GemmArgs g = base_args(m, n, k, scale, c);
+    g.words = mask->words;
+    g.mask_cols = mask->block_cols;
+    g.out_col_blk = mask->k_blk;
+    g.out_row_blk = mask->m_blk;
+    g.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
+    g.counters = counters;
+    const CUtensorMap tb = b_kmajor ? kmajor_map(b, k, n) : mnmajor_map(b, n, k);
+    launch_gemm(false, !b_kmajor, GemmKind::sdd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m), tb,
+                out_map(c, c_dtype, m, n), g, as_stream(stream));
+}
+
+int sd_sdd_matmul(const void* a, const void* b, const sd_block_mask* mask, float scale, void* c,
+                  int32_t c_dtype, int32_t m, int32_t n, int32_t k, unsigned long long* counters,
+                  void* stream) {
+    return guarded([&] { sdd(a, b, false, mask, scale, c, c_dtype, m, n, k, counters, stream, "sdd_matmul"); });
+}
+
+// layer.hpp:158: dx (m x k) = s * (dy (m x n) * W^T) (.) m, W (k x n) read in place.
+int sd_linear_backward_dx(const void* dy, const void* w, const sd_block_mask* mask, float scale, void* dx,
+                          int32_t dx_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
+    return guarded([&] {
+        // the sdd problem is (M, K_out = k, N_red = n)
+        sdd(dy, w, true, mask, scale, dx, dx_dtype, m, k, n, nullptr, stream, "layer backward dx");
+    });
+}
+
+// layer.hpp:159-160: dw (k x n) = s * (x (.) m)^T dy over the column lists of m.
+int sd_linear_backward_dw(const void* x, const sd_block_mask* mask, const void* dy, float scale, void* dw,
+                          int32_t dw_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
+    return guarded([&] {
+        // the dsd problem is (K_out = k rows, N, M_red = m)
+        check_gemm(k, n, m);
+        check_ptr(x, "x"), check_ptr(dy, "dy"), check_ptr(dw, "dw"), check_dtype(dw_dtype);
+        if (!mask) fail(SD_EINVAL, "layer backward dw: null mask");
+        check_divides(mask->m_blk, m, "m_blk");
+        check_divides(mask->k_blk, k, "k_blk");
+        check_mask_geometry(mask, m / mask->m_blk, k / mask->k_blk, mask->m_blk, mask->k_blk,
+                            "layer backward dw");
+        check_row_blk(mask->k_blk, "k_blk");
+        check_red_blk(mask->m_blk, "m_blk");
+        require_device();
+        GemmArgs g = base_args(k, n, m, scale, dw);
+        g.list_cnt = mask->col_cnt;
+        g.list_idx = mask->col_idx;
+        g.list_stride = mask->block_rows;
+        g.red_blk = mask->m_blk;
+        g.out_row_blk = mask->k_blk;
+        g.row_order = mask->k_blk == kBM ? mask->col_order : nullptr;
+        launch_gemm(true, true, GemmKind::dsd, dw_dtype == SD_DTYPE_F32, mnmajor_map(x, k, m),
+                    mnmajor_map(dy, n, m), out_map(dw, dw_dtype, k, n), g, as_stream(stream));
+    });
+}
+
+uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k) { return 2ull * m * n * k; }
+
+uint64_t sd_flops_effective(int64_t n, int64_t k, int32_t m_blk, int32_t n_blk, int32_t k_blk, int64_t keep,
+                            int32_t kind) {
+    const uint64_t kp = static_cast<uint64_t>(keep);
+    if (kind == 0) return 2ull * static_cast<uint64_t>(n) * m_blk * k_blk * kp;
+    return 2ull * static_cast<uint64_t>(k) * m_blk * n_blk * kp;
+}
+
+}  // extern "C"

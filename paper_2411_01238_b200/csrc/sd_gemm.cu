@@ -1,0 +1,400 @@
+// sd_gemm.cu — the SparseDrop tensor-core GEMMs for sm_100a.
+//
+// One persistent, warp-specialised tcgen05 kernel, templated on operand
+// major-ness and on how the block mask enters, serves every GEMM of the path:
+//
+//   dsd (reduction-block skipping, gemm.hpp:133-170):
+//     forward  Y  = s (X (.) m) W      A = X  K-major, B = W  MN-major, row lists
+//     dW       dW = s (X (.) m)^T dY   A = X  MN-major, B = dY MN-major, column lists
+//     dense    (list == null: every reduction block)
+//   sdd (output-block skipping, gemm.hpp:176-213):
+//     dX       dX = s (dY W^T) (.) m   A = dY K-major, B = W  K-major, mask bits
+//
+// Tile: 128 output rows (one tcgen05 M=128 MMA, TMEM lanes = rows) x up to 256
+// output columns (MMA N chosen per tile at run time: 256, or 128 for a ragged
+// edge / a half-kept sdd pair). Reduction in 64-element stages = one 128-byte
+// swizzle atom; a 128-wide mask block is two stages (the paper's retile(1,2),
+// PAPER.md:149-151). Only kept reduction blocks are ever loaded by TMA.
+//
+// Warp roles (256 threads, 1 CTA per SM, grid = min(units, #SMs)):
+//   warp 0      TMA producer (one lane): 4-stage smem ring, mbarrier full/empty
+//   warp 1      MMA issuer (one lane): tcgen05.mma -> TMEM, tcgen05.commit
+//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  epilogue: tcgen05.ld -> scale -> bf16/fp32 -> swizzled smem
+//               -> TMA store; all-dropped tiles written as +0.0 directly.
+// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
+// Every role walks the same static unit sequence (u = blockIdx.x + i*gridDim.x),
+// so no scheduling state crosses roles; zero-work units skip TMEM entirely.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "sd_internal.h"
+#include "sd_ptx.cuh"
+
+namespace sd {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
+constexpr int kBBytes = kBN * kBK * 2;  // 32 KB per stage
+constexpr int kEpiWarps = 4;
+constexpr int kEpiBufBytes = 32 * 128;  // one warp's 32 rows x 128 B store box
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+
+constexpr int kOffA = 0;
+constexpr int kOffB = kOffA + kStages * kABytes;
+constexpr int kOffEpi = kOffB + kStages * kBBytes;
+constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+constexpr int kNumBars = 2 * kStages + 4;
+constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
+constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
+
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+struct Unit {
+    int row0;      // first output row
+    int list_row;  // mask row (list index) of this tile row
+    int n0;        // first output column (dsd)
+    int n_eff;     // MMA N; 0 => no MMA work
+    int nstages;   // reduction stages
+    int nslots;    // sdd: kept output blocks in this unit
+    int slot_blk[2];
+    int nzero;     // sdd: dropped output blocks in this unit
+    int zero_blk[2];
+};
+
+template <bool SDD>
+__device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
+    Unit t;
+    const int i = u / a.n_col_units;
+    const int cu = u - i * a.n_col_units;
+    const int rt = a.row_order ? __ldg(a.row_order + i) : i;
+    t.row0 = rt * kBM;
+    t.list_row = t.row0 / a.out_row_blk;
+    t.nslots = 0;
+    t.nzero = 0;
+    if constexpr (!SDD) {
+        t.n0 = cu * kBN;
+        const int rem = a.cols_out - t.n0;
+        t.n_eff = rem < kBN ? rem : kBN;
+        const int cnt = a.list_cnt ? __ldg(a.list_cnt + t.list_row) : a.red / a.red_blk;
+        t.nstages = cnt * (a.red_blk / kBK);
+        if (cnt == 0) t.n_eff = 0;
+    } else {
+        const int per_unit = kBN / a.out_col_blk;
+        const int b0 = cu * per_unit;
+        const int nb = min(per_unit, a.mask_cols - b0);
+        t.n0 = b0 * a.out_col_blk;
+        for (int j = 0; j < nb; ++j) {
+            const int64_t b = static_cast<int64_t>(t.list_row) * a.mask_cols + b0 + j;
+            const bool kept = (__ldg(a.words + (b >> 6)) >> (b & 63)) & 1ull;
+            if (kept)
+                t.slot_blk[t.nslots++] = b0 + j;
+            else
+                t.zero_blk[t.nzero++] = b0 + j;
+        }
+        t.n_eff = t.nslots * a.out_col_blk;
+        t.nstages = a.red / kBK;
+    }
+    return t;
+}
+
+// Zero a 32-row x `ncols` slab of the output with coalesced 16-byte stores.
+template <bool OUT_F32>
+__device__ __forceinline__ void zero_rows(const GemmArgs& a, int row_first, int col0, int ncols,
+                                          uint32_t lane) {
+    constexpr int kElem = OUT_F32 ? 4 : 2;
+    const int chunks_per_row = ncols * kElem / 16;
+    const int total = 32 * chunks_per_row;
+    char* base = static_cast<char*>(a.out);
+    for (int idx = lane; idx < total; idx += 32) {
+        const int r = idx / chunks_per_row;
+        const int ch = idx - r * chunks_per_row;
+        char* p = base + (static_cast<int64_t>(row_first + r) * a.cols_out + col0) * kElem + ch * 16;
+        ptx::st_global_v4_zero(p);
+    }
+}
+
+template <bool A_MN, bool B_MN, bool SDD, bool OUT_F32>
+__global__ void __launch_bounds__(kThreads, 1)
+    sd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmOut, const GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+    const uint32_t sbase = ptx::smem_u32(smem);
+
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+
+    const uint32_t warp = threadIdx.x / 32;
+    const uint32_t lane = ptx::lane_id();
+    const int num_units = args.n_row_tiles * args.n_col_units;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmOut);
+        for (int i = 0; i < kStages; ++i) {
+            ptx::mbar_init(full_bar + i, 1);
+            ptx::mbar_init(empty_bar + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(tfull_bar + i, 1);
+            ptx::mbar_init(tempty_bar + i, kEpiWarps);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+                const Unit t = decode_unit<SDD>(args, u);
+                if (t.n_eff == 0) continue;
+                const uint32_t tx_bytes = kABytes + t.n_eff * kBK * 2;
+                const int spb = args.red_blk / kBK;
+                for (int s = 0; s < t.nstages; ++s) {
+                    int r0;
+                    if constexpr (!SDD) {
+                        const int li = s / spb;
+                        const int kb = args.list_idx
+                                           ? __ldg(args.list_idx +
+                                                   static_cast<int64_t>(t.list_row) * args.list_stride + li)
+                                           : li;
+                        r0 = kb * args.red_blk + (s - li * spb) * kBK;
+                    } else {
+                        r0 = s * kBK;
+                    }
+                    ptx::mbar_wait(empty_bar + stage, phase ^ 1);
+                    uint64_t* fb = full_bar + stage;
+                    ptx::mbar_arrive_expect_tx(fb, tx_bytes);
+                    uint8_t* sA = smem + kOffA + stage * kABytes;
+                    uint8_t* sB = smem + kOffB + stage * kBBytes;
+                    if constexpr (!A_MN) {
+                        ptx::tma_load_2d(&tmA, fb, sA, r0, t.row0, pol);
+                    } else {
+                        ptx::tma_load_2d(&tmA, fb, sA, t.row0, r0, pol);
+                        ptx::tma_load_2d(&tmA, fb, sA + 8192, t.row0 + 64, r0, pol);
+                    }
+                    if constexpr (!SDD) {
+                        if constexpr (!B_MN) {
+                            for (int j = 0; j < t.n_eff / 128; ++j)
+                                ptx::tma_load_2d(&tmB, fb, sB + j * 16384, r0, t.n0 + 128 * j, pol);
+                        } else {
+                            for (int j = 0; j < t.n_eff / 64; ++j)
+                                ptx::tma_load_2d(&tmB, fb, sB + j * 8192, t.n0 + 64 * j, r0, pol);
+                        }
+                    } else {
+                        for (int sl = 0; sl < t.nslots; ++sl) {
+                            const int col0 = t.slot_blk[sl] * args.out_col_blk;
+                            if constexpr (!B_MN) {
+                                const int per = args.out_col_blk / 128;
+                                for (int j = 0; j < per; ++j)
+                                    ptx::tma_load_2d(&tmB, fb, sB + (sl * per + j) * 16384, r0,
+                                                     col0 + 128 * j, pol);
+                            } else {
+                                const int per = args.out_col_blk / 64;
+                                for (int j = 0; j < per; ++j)
+                                    ptx::tma_load_2d(&tmB, fb, sB + (sl * per + j) * 8192,
+                                                     col0 + 64 * j, r0, pol);
+                            }
+                        }
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t acc_iter = 0;
+            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+                const Unit t = decode_unit<SDD>(args, u);
+                if (t.n_eff == 0) continue;
+                const uint32_t acc = acc_iter & 1;
+                const uint32_t acc_phase = (acc_iter >> 1) & 1;
+                ++acc_iter;
+                ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kBN;
+                const uint32_t idesc = ptx::make_idesc_bf16(kBM, t.n_eff, A_MN, B_MN);
+                for (int s = 0; s < t.nstages; ++s) {
+                    ptx::mbar_wait(full_bar + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = sbase + kOffA + stage * kABytes;
+                    const uint32_t b_addr = sbase + kOffB + stage * kBBytes;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t ad = A_MN ? ptx::make_sw128_desc(a_addr + k * 2048, 8192, 1024)
+                                                 : ptx::make_sw128_desc(a_addr + k * 32, 0, 1024);
+                        const uint64_t bd = B_MN ? ptx::make_sw128_desc(b_addr + k * 2048, 8192, 1024)
+                                                 : ptx::make_sw128_desc(b_addr + k * 32, 0, 1024);
+                        ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    }
+                    ptx::mma_commit(empty_bar + stage);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(tfull_bar + acc);
+                if (args.counters)
+                    atomicAdd(args.counters + t.row0 / kBM,
+                              static_cast<unsigned long long>(t.nstages / 2) * (t.n_eff / 128));
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue =====================
+        const uint32_t q = warp & 3;  // TMEM lane quarter == output row quarter
+        uint8_t* ebuf = smem + kOffEpi + q * 2 * kEpiBufBytes;
+        const uint32_t ebuf_addr = sbase + kOffEpi + q * 2 * kEpiBufBytes;
+        uint32_t bi = 0;
+        uint32_t acc_iter = 0;
+        constexpr int kChunkCols = OUT_F32 ? 32 : 64;  // 128 bytes of output per row
+        for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            const Unit t = decode_unit<SDD>(args, u);
+            const int row_first = t.row0 + 32 * q;
+            if constexpr (SDD) {
+                for (int z = 0; z < t.nzero; ++z)
+                    zero_rows<OUT_F32>(args, row_first, t.zero_blk[z] * args.out_col_blk,
+                                       args.out_col_blk, lane);
+            }
+            if (t.n_eff == 0) {
+                if constexpr (!SDD) {
+                    const int rem = args.cols_out - t.n0;
+                    zero_rows<OUT_F32>(args, row_first, t.n0, rem < kBN ? rem : kBN, lane);
+                }
+                continue;
+            }
+            const uint32_t acc = acc_iter & 1;
+            const uint32_t acc_phase = (acc_iter >> 1) & 1;
+            ++acc_iter;
+            ptx::mbar_wait(tfull_bar + acc, acc_phase);
+            ptx::tc_fence_after();
+            const int nchunks = t.n_eff / kChunkCols;
+            for (int c = 0; c < nchunks; ++c) {
+                const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kBN + c * kChunkCols;
+                uint32_t v[kChunkCols];
+                ptx::tmem_ld_32x32b_x32(taddr, v);
+                if constexpr (!OUT_F32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
+                ptx::tmem_ld_wait();
+                if (c == nchunks - 1) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(tempty_bar + acc);
+                }
+                // staging buffer bi must no longer be read by the TMA store issued 2 chunks ago
+                if (lane == 0) ptx::bulk_wait_group_read<1>();
+                __syncwarp();
+                const uint32_t row_addr = ebuf_addr + bi * kEpiBufBytes + lane * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t w0, w1, w2, w3;
+                    if constexpr (OUT_F32) {
+                        w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * args.scale);
+                        w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * args.scale);
+                        w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * args.scale);
+                        w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * args.scale);
+                    } else {
+                        const float* f = reinterpret_cast<const float*>(v) + 8 * j;
+                        w0 = ptx::pack_bf16x2(f[0] * args.scale, f[1] * args.scale);
+                        w1 = ptx::pack_bf16x2(f[2] * args.scale, f[3] * args.scale);
+                        w2 = ptx::pack_bf16x2(f[4] * args.scale, f[5] * args.scale);
+                        w3 = ptx::pack_bf16x2(f[6] * args.scale, f[7] * args.scale);
+                    }
+                    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), w0, w1, w2, w3);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    int col;
+                    if constexpr (SDD) {
+                        const int tcol = c * kChunkCols;
+                        const int sl = tcol / args.out_col_blk;
+                        col = t.slot_blk[sl] * args.out_col_blk + (tcol - sl * args.out_col_blk);
+                    } else {
+                        col = t.n0 + c * kChunkCols;
+                    }
+                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
+                    ptx::bulk_commit_group();
+                }
+                bi ^= 1;
+            }
+        }
+        if (lane == 0) ptx::bulk_wait_group<0>();
+        __syncwarp();
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+template <bool A_MN, bool B_MN, bool SDD, bool OUT_F32>
+void launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout,
+                 const GemmArgs& args, cudaStream_t s) {
+    auto kern = sd_gemm_kernel<A_MN, B_MN, SDD, OUT_F32>;
+    static bool configured = false;  // per instantiation; attribute is per-function
+    if (!configured) {
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes),
+                   "cudaFuncSetAttribute(max dynamic smem)");
+        configured = true;
+    }
+    const int units = args.n_row_tiles * args.n_col_units;
+    const int grid = units < num_sms() ? units : num_sms();
+    if (grid <= 0) return;
+    kern<<<grid, kThreads, kSmemBytes, s>>>(ta, tb, tout, args);
+    check_cuda(cudaGetLastError(), "sd_gemm_kernel launch");
+    note_launch();
+}
+
+}  // namespace
+
+void launch_gemm(bool a_mn, bool b_mn, GemmKind kind, bool out_f32, const CUtensorMap& ta,
+                 const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& args,
+                 cudaStream_t s) {
+    const bool sdd = kind == GemmKind::sdd;
+#define SD_DISPATCH(AM, BM_, SD_, F32)                                                    \
+    if (a_mn == AM && b_mn == BM_ && sdd == SD_ && out_f32 == F32)                        \
+        return launch_impl<AM, BM_, SD_, F32>(ta, tb, tout, args, s);
+    // dsd / dense forward (X K-major, W MN-major)
+    SD_DISPATCH(false, true, false, false)
+    SD_DISPATCH(false, true, false, true)
+    // dsd dW (X^T MN-major, dY MN-major) and dense x^T dy
+    SD_DISPATCH(true, true, false, false)
+    SD_DISPATCH(true, true, false, true)
+    // dense dy W^T (both K-major)
+    SD_DISPATCH(false, false, false, false)
+    SD_DISPATCH(false, false, false, true)
+    // sdd dX in the layer (dY K-major, W K-major)
+    SD_DISPATCH(false, false, true, false)
+    SD_DISPATCH(false, false, true, true)
+    // sdd reference form (a K-major, b row-major = MN-major)
+    SD_DISPATCH(false, true, true, false)
+    SD_DISPATCH(false, true, true, true)
+#undef SD_DISPATCH
+    fail(SD_EINVAL, "unsupported GEMM operand layout combination");
+}
+
+}  // namespace sd

@@ -1,0 +1,280 @@
+// sd_mask.cu — block-mask generation and compaction (one launch).
+//
+// K1 (sample_mask, block_mask.cpp:52-80): the keep bit of block (r, c) is the
+//     reference's splitmix64 counter hash, keep iff
+//       unit_interval(counter_hash(seed, r, c)) >= p
+//     evaluated exactly in integers: (h >> 11) >= ceil(p * 2^53). The decision
+//     depends only on (seed, r, c), so a row shard hashes its GLOBAL rows
+//     r0 + r and is bit-identical to the matching rows of the global mask.
+// K2 (kept_blocks_in_row, block_mask.cpp:125-135, on the mask and on
+//     transpose_mask, :117-123): warp-ballot compaction, one warp per block row
+//     (row lists) and one warp per block column (column lists); positions are
+//     the popcount of the ballot below the lane, so lists come out strictly
+//     increasing like the reference's.
+// The three parts read nothing but (seed, r, c) — each recomputes the hash — so
+// they run as independent blocks of a single grid; the last block to finish
+// (threadfence + ticket) reduces keep_count and builds the cost-ordered row /
+// column permutations the persistent GEMM scheduler walks (heaviest first).
+// All of this is latency-bound integer work (a 512x64 grid is 4 KB of words).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "sd_internal.h"
+
+namespace sd {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxOrderBins = 8192;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+struct PlanArgs {
+    sd_block_mask m;
+    int from_words;
+    uint64_t seed_mix;   // mix64(seed): counter_hash = mix64(mix64(seed_mix ^ r) ^ c)
+    uint64_t threshold;  // ceil(p * 2^53)
+    int nb_words, nb_rows, nb_cols;
+};
+
+__device__ __forceinline__ bool keep_bit(const PlanArgs& a, int r, int c) {
+    if (a.from_words) {
+        const int64_t b = static_cast<int64_t>(r) * a.m.block_cols + c;
+        return (a.m.words[b >> 6] >> (b & 63)) & 1ull;
+    }
+    const uint64_t h =
+        mix64(mix64(a.seed_mix ^ static_cast<uint64_t>(r + a.m.row_block_offset)) ^ static_cast<uint64_t>(c));
+    return (h >> 11) >= a.threshold;
+}
+
+// Exclusive scan of n ints in smem, DESCENDING index order:
+// out[v] = sum_{w > v} in[v]. 256 threads.
+__device__ void scan_desc(int* bins, int n, int* warp_tot) {
+    const int tid = threadIdx.x;
+    const int per = (n + kThreads - 1) / kThreads;
+    // thread t owns reversed positions [t*per, t*per+per): index n-1-pos
+    int local = 0;
+    for (int i = 0; i < per; ++i) {
+        const int pos = tid * per + i;
+        if (pos < n) local += bins[n - 1 - pos];
+    }
+    // block exclusive scan of `local`
+    const int lane = tid & 31, wid = tid >> 5;
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < kThreads / 32 ? warp_tot[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
+        }
+        if (lane < kThreads / 32) warp_tot[lane] = w;  // inclusive warp prefix
+    }
+    __syncthreads();
+    int run = incl - local + (wid > 0 ? warp_tot[wid - 1] : 0);
+    for (int i = 0; i < per; ++i) {
+        const int pos = tid * per + i;
+        if (pos < n) {
+            const int idx = n - 1 - pos;
+            const int v = bins[idx];
+            bins[idx] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+}
+
+// Counting sort of `count` (values in [0, max_val]) into a descending order.
+__device__ void order_by_count(const int32_t* count, int n, int max_val, int32_t* order, int* bins,
+                               int* warp_tot) {
+    if (max_val + 1 > kMaxOrderBins) {
+        for (int i = threadIdx.x; i < n; i += kThreads) order[i] = i;
+        return;
+    }
+    const int nb = max_val + 1;
+    for (int i = threadIdx.x; i < nb; i += kThreads) bins[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&bins[__ldcg(count + i)], 1);
+    __syncthreads();
+    scan_desc(bins, nb, warp_tot);
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+        const int pos = atomicAdd(&bins[__ldcg(count + i)], 1);
+        order[pos] = i;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
+    extern __shared__ int dyn_smem[];
+    __shared__ int warp_tot[kThreads / 32];
+    __shared__ unsigned long long keep_part[kThreads / 32];
+    __shared__ bool is_last;
+    const int R = a.m.block_rows, C = a.m.block_cols;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    int blk = blockIdx.x;
+
+    if (blk < a.nb_words) {
+        // ---- words: one thread per 64-bit word (hash mode only)
+        const int64_t total = static_cast<int64_t>(R) * C;
+        const int64_t nwords = (total + 63) / 64;
+        const int64_t w = static_cast<int64_t>(blk) * kThreads + threadIdx.x;
+        if (w < nwords) {
+            int64_t b = w * 64;
+            int r = static_cast<int>(b / C), c = static_cast<int>(b % C);
+            uint64_t word = 0;
+            for (int i = 0; i < 64 && b < total; ++i, ++b) {
+                word |= static_cast<uint64_t>(keep_bit(a, r, c)) << i;
+                if (++c == C) {
+                    c = 0;
+                    ++r;
+                }
+            }
+            a.m.words[w] = word;
+        }
+    } else if ((blk -= a.nb_words) < a.nb_rows) {
+        // ---- row lists: one warp per block row
+        const int r = blk * (kThreads / 32) + wid;
+        if (r < R) {
+            int base = 0;
+            int32_t* dst = a.m.row_idx + static_cast<int64_t>(r) * C;
+            for (int c0 = 0; c0 < C; c0 += 32) {
+                const int c = c0 + lane;
+                const bool k = c < C && keep_bit(a, r, c);
+                const uint32_t bal = __ballot_sync(0xffffffffu, k);
+                if (k) dst[base + __popc(bal & lt)] = c;
+                base += __popc(bal);
+            }
+            if (lane == 0) a.m.row_cnt[r] = base;
+        }
+    } else {
+        // ---- column lists: one warp per block column
+        blk -= a.nb_rows;
+        const int c = blk * (kThreads / 32) + wid;
+        if (c < C) {
+            int base = 0;
+            int32_t* dst = a.m.col_idx + static_cast<int64_t>(c) * R;
+            for (int r0 = 0; r0 < R; r0 += 32) {
+                const int r = r0 + lane;
+                const bool k = r < R && keep_bit(a, r, c);
+                const uint32_t bal = __ballot_sync(0xffffffffu, k);
+                if (k) dst[base + __popc(bal & lt)] = r;
+                base += __popc(bal);
+            }
+            if (lane == 0) a.m.col_cnt[c] = base;
+        }
+    }
+
+    // ---- last block: keep_count and cost orders
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(a.m.ticket, 1u);
+        is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+
+    unsigned long long kc = 0;
+    for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(__ldcg(a.m.row_cnt + r));
+    for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+    if (lane == 0) keep_part[wid] = kc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int i = 0; i < kThreads / 32; ++i) s += keep_part[i];
+        *a.m.keep_count = static_cast<int64_t>(s);
+    }
+    order_by_count(a.m.row_cnt, R, C, a.m.row_order, dyn_smem, warp_tot);
+    order_by_count(a.m.col_cnt, C, R, a.m.col_order, dyn_smem, warp_tot);
+    if (threadIdx.x == 0) *a.m.ticket = 0u;  // re-arm for the next launch on this workspace
+}
+
+__device__ __forceinline__ bool in_bit(const uint64_t* w, int64_t b) { return (w[b >> 6] >> (b & 63)) & 1ull; }
+
+// transpose_mask (block_mask.cpp:117-123): out bit (c, r) = in bit (r, c).
+__global__ void mask_transpose_kernel(const uint64_t* in, int R, int C, uint64_t* out) {
+    const int64_t total = static_cast<int64_t>(R) * C;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w >= (total + 63) / 64) return;
+    uint64_t word = 0;
+    for (int i = 0; i < 64; ++i) {
+        const int64_t b = w * 64 + i;  // bit of the (C x R) output grid
+        if (b >= total) break;
+        const int64_t c = b / R, r = b % R;
+        word |= static_cast<uint64_t>(in_bit(in, r * C + c)) << i;
+    }
+    out[w] = word;
+}
+
+// retile (block_mask.cpp:100-115): out bit (r, c) = in bit (r / sm, c / sk).
+__global__ void mask_retile_kernel(const uint64_t* in, int R, int C, int sm, int sk, uint64_t* out) {
+    const int R2 = R * sm, C2 = C * sk;
+    const int64_t total = static_cast<int64_t>(R2) * C2;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w >= (total + 63) / 64) return;
+    uint64_t word = 0;
+    for (int i = 0; i < 64; ++i) {
+        const int64_t b = w * 64 + i;
+        if (b >= total) break;
+        const int64_t r = b / C2, c = b % C2;
+        word |= static_cast<uint64_t>(in_bit(in, (r / sm) * C + c / sk)) << i;
+    }
+    out[w] = word;
+}
+
+}  // namespace
+
+void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix, uint64_t threshold,
+                      cudaStream_t s) {
+    PlanArgs a;
+    a.m = m;
+    a.from_words = from_words ? 1 : 0;
+    a.seed_mix = seed_mix;
+    a.threshold = threshold;
+    const int64_t nwords = (static_cast<int64_t>(m.block_rows) * m.block_cols + 63) / 64;
+    a.nb_words = from_words ? 0 : static_cast<int>((nwords + kThreads - 1) / kThreads);
+    a.nb_rows = (m.block_rows + kThreads / 32 - 1) / (kThreads / 32);
+    a.nb_cols = (m.block_cols + kThreads / 32 - 1) / (kThreads / 32);
+    const int grid = a.nb_words + a.nb_rows + a.nb_cols;
+    const int bins = std::min(std::max(m.block_rows, m.block_cols) + 1, kMaxOrderBins);
+    const size_t smem = static_cast<size_t>(bins) * sizeof(int);
+    mask_plan_kernel<<<grid, kThreads, smem, s>>>(a);
+    check_cuda(cudaGetLastError(), "mask_plan_kernel launch");
+    note_launch();
+}
+
+void launch_mask_transpose(const sd_block_mask& in, sd_block_mask& out, cudaStream_t s) {
+    const int64_t nwords = (static_cast<int64_t>(in.block_rows) * in.block_cols + 63) / 64;
+    const int grid = static_cast<int>((nwords + kThreads - 1) / kThreads);
+    mask_transpose_kernel<<<grid, kThreads, 0, s>>>(in.words, in.block_rows, in.block_cols, out.words);
+    check_cuda(cudaGetLastError(), "mask_transpose_kernel launch");
+    note_launch();
+    launch_mask_plan(out, true, 0, 0, s);
+}
+
+void launch_mask_retile(const sd_block_mask& in, int split_m, int split_k, sd_block_mask& out,
+                        cudaStream_t s) {
+    const int64_t nwords =
+        (static_cast<int64_t>(out.block_rows) * out.block_cols + 63) / 64;
+    const int grid = static_cast<int>((nwords + kThreads - 1) / kThreads);
+    mask_retile_kernel<<<grid, kThreads, 0, s>>>(in.words, in.block_rows, in.block_cols, split_m,
+                                                 split_k, out.words);
+    check_cuda(cudaGetLastError(), "mask_retile_kernel launch");
+    note_launch();
+    launch_mask_plan(out, true, 0, 0, s);
+}
+
+}  // namespace sd
