@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""bench.py — SparseDrop fwd+bwd on B200 (BASELINE.json metric, configs[1]).
+
+One step = one SparseDrop linear layer training step on the hot path:
+  K1+K2 mask generation + compaction (fresh draw, seed varies per step)
+  K4 forward  Y  = s (X (.) m) W         (dsd, dropped K-blocks never read)
+  K6 backward dW = s (X (.) m)^T dY       (dsd over mask columns)
+  [N > 1: NCCL all-reduce of dW on a side stream, overlapped with dX]
+  K5 backward dX = s (dY W^T) (.) m       (sdd, dropped output tiles = +0.0)
+at M=N=K=4096 per GPU (configs[1]), 128x128 blocks, headline p = 0.5, with the
+p = 0.0..0.9 sweep and our own dense tcgen05 fwd+bwd (same kernel, no mask) as
+the speed-up denominator. Row-sharded data parallel for N > 1 (weak scaling:
+each rank owns 4096 rows of M; masks are generated shard-locally from the
+global block-row index, bit-identical with the global mask; W is replicated).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference, else the oracle port) on the host cores.
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SparseDrop fwd+bwd TFLOP/s (dense-equiv) & speedup vs dense GEMM vs p"
+UNIT = "TFLOP/s"
+SWEEP_P = [0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9]
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=4096, help="M (per GPU) = N = K")
+    ap.add_argument("--p", type=float, default=0.5, help="headline drop rate")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (headline loop only)")
+    return ap.parse_args()
+
+
+def workload_config(size, p, world):
+    return {
+        "workload": f"configs[1]: SparseDrop linear fwd+bwd (mask gen + dsd fwd + dsd dW + sdd dX), "
+                    f"M={size}/GPU, N=K={size}, 128x128 blocks, p={p} (sweep p=0..0.9 in 'sweep')",
+        "M_per_gpu": size, "N": size, "K": size, "M_global": size * world,
+        "m_blk": 128, "k_blk": 128, "p": p, "seed": 0,
+        "dtypes": {"x/w/dy/y/dx": "bf16", "dw": "fp32", "accumulate": "fp32"},
+        "l2": "flushed between timed steps (512 MiB device write outside the timed events)",
+        "parallelism": f"dp{world} row-sharded (shard-local masks, dW all-reduce)" if world > 1 else "single GPU",
+    }
+
+
+# ------------------------------------------------------------------ CPU legs (reference / oracle)
+
+def _cpu_layer_runner():
+    """-> (kind, fn(x, w, dy, p, threads)) timing the reference's layer fwd+bwd."""
+    import numpy as np
+
+    from oracle.oracle import ORACLE_LIB, REF_LIB, Oracle, Reference
+
+    if REF_LIB.exists():
+        ref = Reference()
+
+        def run(x, w, dy, p, threads):
+            ref.layer_fwd_bwd(x, w, dy, p, 128, 128, 128, seed=0, step_seed=0, layer_index=0, threads=threads,
+                              dtype=np.float32)
+
+        return "reference", run
+    if not ORACLE_LIB.exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "all"], check=True, stdout=subprocess.DEVNULL)
+    o = Oracle()
+
+    def run(x, w, dy, p, threads):
+        eff = o.effective_seed(0, 0, 0)
+        words, _ = o.sample_mask(p, 128, 128, eff, x.shape[0], x.shape[1])
+        s = 1.0 / (1.0 - p)
+        o.dsd_matmul(x, words, w, 128, 128, 128, s, threads=threads)
+        o.layer_dw(x, dy, words, 128, 128, s, threads=threads)
+        o.layer_dx(dy, w, words, 128, 128, s, threads=threads)
+
+    return "port", run
+
+
+def cpu_sample_inputs(size, n_slab):
+    """The configs[1] problem restricted to an N-column slab: M=K=size, N=n_slab.
+    Work is linear in N, and the reference's tile-row parallelism (M/128 rows for
+    fwd/dX, K/128 for dW) is unchanged by the slab."""
+    from oracle.oracle import Oracle
+
+    o = Oracle()
+    bf = lambda r, c, s: o.bf16_bits_to_f64(o.to_bf16_bits(o.random_matrix(r, c, s))).astype("float32")
+    return bf(size, size, 1), bf(size, n_slab, 2), bf(size, n_slab, 3)
+
+
+def cpu_baseline(size, p, budget_s=12.0):
+    threads = os.cpu_count() or 1
+    kind, run = _cpu_layer_runner()
+    n_slab = max(128, min(size, 512))
+    x, w, dy = cpu_sample_inputs(size, n_slab)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 or (time.perf_counter() - t_start < budget_s and len(times) < 20):
+        t0 = time.perf_counter()
+        run(x, w, dy, p, threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > 4 * budget_s:
+            break
+    t = sorted(times)[len(times) // 2]
+    flops = 3 * 2 * size * n_slab * size
+    return {
+        "value": flops / t / 1e12, "unit": UNIT, "cores": threads, "kind": kind,
+        "sample": f"layer fwd+bwd (sample_mask+dsd fwd+sdd dX+dsd dW, float) at M=K={size}, N-column slab "
+                  f"{n_slab} of {size} (work linear in N), p={p}, median of {len(times)} runs, "
+                  f"{threads} threads; dense-equivalent FLOP/s",
+        "seconds_per_sample": t,
+    }
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    kind, run = _cpu_layer_runner()
+    n_slab = max(128, min(args.size, 512))
+    x, w, dy = cpu_sample_inputs(args.size, n_slab)
+    for _ in range(args.warmup):
+        run(x, w, dy, args.p, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run(x, w, dy, args.p, threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    flops = 3 * 2 * args.size * n_slab * args.size
+    value = flops / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference random_matrix)",
+        "config": workload_config(args.size, args.p, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"per step: the reference layer fwd+bwd at M=K={args.size}, N-column slab "
+                                   f"{n_slab} (work linear in N), {threads} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        s = sorted(sm)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_01238_b200 as sd
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    S = args.size
+    M, N, K = S, S, S
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def synth(r, c):
+        # random_matrix's distribution (oracles.hpp:31-41): |v| in [0.25, 1.25), random sign
+        u = torch.rand(r, c, generator=gen, device=dev)
+        sign = torch.where(torch.rand(r, c, generator=gen, device=dev) < 0.5, -1.0, 1.0)
+        return ((0.25 + u) * sign).to(torch.bfloat16)
+
+    x = synth(M, K)
+    gen_w = torch.Generator(device=dev)
+    gen_w.manual_seed(99)  # W replicated: same on every rank
+    w = ((0.25 + torch.rand(K, N, generator=gen_w, device=dev)) *
+         torch.where(torch.rand(K, N, generator=gen_w, device=dev) < 0.5, -1.0, 1.0)).to(torch.bfloat16)
+    dy = synth(M, N)
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    comm = torch.cuda.Stream(device=dev) if world > 1 else None
+    row_off = rank * (M // 128)
+
+    def flush():
+        flush_buf.fill_(float(len(str(flush_buf.numel()))))
+
+    def time_steps(step, steps, warmup):
+        """Sum of per-step CUDA-event durations on the launching stream (L2 flushed
+        before every step, outside the events); max over ranks."""
+        for i in range(warmup):
+            flush()
+            step(i)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        l0 = sd.launch_count()
+        for i in range(steps):
+            flush()
+            evs[i][0].record()
+            step(warmup + i)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launch_box[0] = sd.launch_count() - l0
+        total_ms = sum(a.elapsed_time(b) for a, b in evs)
+        return max_over_ranks(total_ms) / steps
+
+    plans = {}
+    launch_box = [0]
+
+    def plan_for(p):
+        if p not in plans:
+            plans[p] = sd.LayerPlan(x, w, dy, p, row_block_offset=row_off)
+        return plans[p]
+
+    def sparse_step_fn(p):
+        plan = plan_for(p)
+
+        def step(i):
+            plan.forward(seed=sd.effective_seed(0, i, 0))
+            if world > 1:
+                plan.backward_dw()
+                comm.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(comm):
+                    dist.all_reduce(plan.dw)
+                plan.backward_dx()
+                torch.cuda.current_stream().wait_stream(comm)
+            else:
+                plan.backward()
+
+        return step
+
+    def dense_step_fn():
+        plan = plan_for(args.p)
+
+        def step(i):
+            plan.dense_forward()
+            if world > 1:
+                plan.dense_backward()  # dw then dx on the compute stream
+                comm.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(comm):
+                    dist.all_reduce(plan.dw)
+                torch.cuda.current_stream().wait_stream(comm)
+            else:
+                plan.dense_backward()
+
+        return step
+
+    def torch_step(i):
+        y = x @ w
+        dw = x.t() @ dy
+        dx = dy @ w.t()
+        return y, dw, dx
+
+    flops_dense_step = 3 * 2 * M * N * K  # per GPU
+
+    # ---- headline: sparse fwd+bwd at args.p
+    head_step = sparse_step_fn(args.p)
+    with ClockSampler(local_rank) as clk:
+        ms = time_steps(head_step, args.steps, args.warmup)
+    gpu_launches = launch_box[0]  # our kernels enqueued inside the timed region (4 per step)
+    plan = plan_for(args.p)
+    keep = plan.mask.keep_count() / plan.mask.total_blocks()
+    value = world * flops_dense_step / (ms * 1e-3) / 1e12
+
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "ms_per_step": ms, "profile": True}),
+                  flush=True)
+        return
+
+    # ---- dense baseline (same kernel, no mask) and cuBLAS for context
+    ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup)
+    ms_torch = time_steps(torch_step, args.steps, args.warmup)
+
+    # ---- per-kernel durations at the headline p (roofline)
+    def kernel_ms(fn, steps):
+        for _ in range(3):
+            flush(); fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); fn(); b.record()
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+        return tot / steps
+
+    keep_blocks = plan.mask.keep_count()
+    exec_flops = 2 * N * 128 * 128 * keep_blocks  # flops_effective (gemm.hpp:222-228), per GEMM
+    kms = {
+        "mask_gen+compact": kernel_ms(lambda: sd.sample_mask(sd.DropoutSpec(args.p, 128, 128, 7), M, K,
+                                                            row_block_offset=row_off, out=plan.mask), args.steps),
+        "dsd_fwd": kernel_ms(lambda: plan.forward(seed=7), args.steps),
+        "dsd_dw": kernel_ms(plan.backward_dw, args.steps),
+        "sdd_dx": kernel_ms(plan.backward_dx, args.steps),
+    }
+    kms["dsd_fwd"] = max(kms["dsd_fwd"] - kms["mask_gen+compact"], 1e-6)  # plan.forward = mask + fwd
+    gemm_k = {k: v for k, v in kms.items() if k != "mask_gen+compact"}
+    dom = max(gemm_k, key=gemm_k.get)
+    achieved = exec_flops / (gemm_k[dom] * 1e-3) / 1e12
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "traffic": traffic, "kernel": dom,
+        "algorithmic_per_launch": {"flops": exec_flops, "note": "keep_count*2*N*128*128 (flops_effective)"},
+        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1590 (B200_PROFILING.md)",
+        "kernel_ms": kms,
+    }
+
+    # ---- sweep
+    sweep = []
+    if not args.no_sweep:
+        for p in SWEEP_P:
+            msp = time_steps(sparse_step_fn(p), max(5, args.steps // 2), 3)
+            pl = plan_for(p)
+            kp = pl.mask.keep_count() / pl.mask.total_blocks()
+            sweep.append({
+                "p": p, "keep": kp, "ms_per_step": msp,
+                "dense_equiv_tflops": world * flops_dense_step / (msp * 1e-3) / 1e12,
+                "executed_tflops": world * kp * flops_dense_step / (msp * 1e-3) / 1e12,
+                "speedup_vs_dense": ms_dense / msp,
+                "time_vs_dense_over_keep": (msp / ms_dense) / max(kp, 1e-9),
+            })
+            if p != args.p:
+                plans.pop(p, None)
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory(); wh = w.cpu().pin_memory(); dyh = dy.cpu().pin_memory()
+        yh = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+        dxh = torch.empty(M, K, dtype=torch.bfloat16).pin_memory()
+        dwh = torch.empty(K, N, dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x); wd = torch.empty_like(w); dyd = torch.empty_like(dy)
+        e2e_plan = sd.LayerPlan(xd, wd, dyd, args.p, row_block_offset=row_off)
+
+        def e2e_step(i):
+            xd.copy_(xh, non_blocking=True); wd.copy_(wh, non_blocking=True); dyd.copy_(dyh, non_blocking=True)
+            e2e_plan.forward(seed=sd.effective_seed(0, i, 0))
+            if world > 1:
+                e2e_plan.backward_dw()
+                dist.all_reduce(e2e_plan.dw)
+                e2e_plan.backward_dx()
+            else:
+                e2e_plan.backward()
+            yh.copy_(e2e_plan.y, non_blocking=True)
+            dxh.copy_(e2e_plan.dx, non_blocking=True)
+            dwh.copy_(e2e_plan.dw, non_blocking=True)
+
+        ms_e2e = time_steps(e2e_step, max(5, args.steps // 2), 2)
+        h2d = (xh.numel() + wh.numel() + dyh.numel()) * 2
+        d2h = yh.numel() * 2 + dxh.numel() * 2 + dwh.numel() * 4
+        e2e = {"value": world * flops_dense_step / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "LayerPlan (C-ABI sd_layer_plan_*) with pinned host buffers, copies on the compute stream"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(S, args.p)
+        except Exception as exc:  # reported, never fatal for the GPU line
+            cpu = {"error": repr(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random_matrix distribution, on device)",
+            "config": workload_config(S, args.p, world),
+            "keep_fraction": keep, "executed_tflops": value * keep,
+            "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
+            "torch_cublas_dense_ms_per_step": ms_torch,
+            "gpu_launches": gpu_launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -153,6 +153,32 @@ SD_API int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_d
 SD_API int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, int32_t m,
                      int32_t n, int32_t k, void* stream); /* c[m,n] = a_t[k,m]^T * b[k,n] */
 
+/* Layer plan: the fused dropout+linear layer of layer.hpp:85-162 with every
+ * operand bound once (tensor maps encoded once, no per-step host work beyond
+ * the launches) — the runtime object a trainer keeps per layer instance.
+ * Buffers: x (m x k), w (k x n), dy (m x n) bf16 inputs; y (m x n), dx (m x k),
+ * dw (k x n) outputs in the given dtypes; `mask` bound with geometry
+ * (m/m_blk) x (k/k_blk) (row_block_offset selects a row shard's global rows).
+ * p fixes the drop rate and the scale float(1/(1-p)) (layer.hpp:78-81).
+ *   forward : sample_mask(seed) + y = s (x (.) m) w          (2 launches)
+ *   backward: dw = s (x (.) m)^T dy, then dx = s (dy w^T) (.) m  (2 launches)
+ * backward_dw / backward_dx split the two so a data-parallel caller can
+ * all-reduce dw on another stream while dx runs. */
+typedef struct sd_layer_plan sd_layer_plan;
+SD_API int sd_layer_plan_create(sd_layer_plan** plan, const void* x, const void* w, const void* dy,
+                                void* y, int32_t y_dtype, void* dx, int32_t dx_dtype, void* dw,
+                                int32_t dw_dtype, int32_t m, int32_t n, int32_t k, double p,
+                                const sd_block_mask* mask);
+SD_API int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream);
+SD_API int sd_layer_plan_backward(sd_layer_plan* plan, void* stream);
+SD_API int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream);
+SD_API int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream);
+/* Dense baseline with the same buffers (layer.hpp:98-99, 140-145): y = x w,
+ * dw = x^T dy, dx = dy w^T on the same tcgen05 kernel, no mask. */
+SD_API int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream);
+SD_API int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream);
+SD_API int sd_layer_plan_destroy(sd_layer_plan* plan);
+
 /* Effective FLOPs (gemm.hpp:217-228): kind 0 = dsd (2*n*m_blk*k_blk*keep),
  * 1 = sdd (2*k*m_blk*n_blk*keep). */
 SD_API uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k);

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     KernelCounters,
     LayerContext,
     LayerGrads,
+    LayerPlan,
     LinearLayer,
     LinearVariant,
     SparseKind,

@@ -64,6 +64,15 @@ PROTOTYPES = {
     "sd_linear_forward": (ctypes.c_int, [_P, _MASKP, _P, ctypes.c_float, _P, _I, _I, _I, _I, _P]),
     "sd_linear_backward_dx": (ctypes.c_int, [_P, _P, _MASKP, ctypes.c_float, _P, _I, _I, _I, _I, _P]),
     "sd_linear_backward_dw": (ctypes.c_int, [_P, _MASKP, _P, ctypes.c_float, _P, _I, _I, _I, _I, _P]),
+    "sd_layer_plan_create": (ctypes.c_int, [ctypes.POINTER(_P), _P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _I, _I,
+                                            ctypes.c_double, _MASKP]),
+    "sd_layer_plan_forward": (ctypes.c_int, [_P, ctypes.c_uint64, _P]),
+    "sd_layer_plan_backward": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_backward_dw": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_backward_dx": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_dense_forward": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
     "sd_flops_dense": (ctypes.c_uint64, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]),
     "sd_flops_effective": (
         ctypes.c_uint64,

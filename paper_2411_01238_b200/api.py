@@ -436,6 +436,74 @@ def backward(layer: LinearLayer, ctx: LayerContext, dy: torch.Tensor, stream=Non
     return LayerGrads(dx, dw)
 
 
+class LayerPlan:
+    """A bound sparsedrop layer (C-ABI sd_layer_plan): buffers and tensor maps are
+    fixed at construction, each step is 2 (forward) + 2 (backward) kernel
+    launches with no host-side work — the runtime object a training loop keeps
+    per layer. Row shards pass `row_block_offset` (global block row of local row 0).
+
+    forward(seed)   : mask = sample_mask(seed) ; y = s (x (.) m) w
+    backward()      : dw = s (x (.) m)^T dy ; dx = s (dy w^T) (.) m
+    """
+
+    def __init__(self, x: torch.Tensor, w: torch.Tensor, dy: torch.Tensor, p: float, m_blk: int = 128,
+                 k_blk: int = 128, row_block_offset: int = 0, y_dtype=torch.bfloat16,
+                 dx_dtype=torch.bfloat16, dw_dtype=torch.float32):
+        _require_bf16("x", x), _require_bf16("w", w), _require_bf16("dy", dy)
+        m, k = x.shape
+        n = w.shape[1]
+        if w.shape[0] != k or dy.shape != (m, n):
+            raise ValueError(f"layer shapes: x {tuple(x.shape)} w {tuple(w.shape)} dy {tuple(dy.shape)}")
+        if m_blk <= 0 or m % m_blk:
+            raise ValueError(f"mask block size m_blk={m_blk} does not divide rows={m}")
+        if k_blk <= 0 or k % k_blk:
+            raise ValueError(f"mask block size k_blk={k_blk} does not divide cols={k}")
+        self.x, self.w, self.dy = x, w, dy
+        self.m, self.n, self.k, self.p = m, n, k, p
+        self.mask = BlockMask(m // m_blk, k // k_blk, m_blk, k_blk, row_block_offset, device=x.device)
+        self.y = torch.empty(m, n, dtype=y_dtype, device=x.device)
+        self.dx = torch.empty(m, k, dtype=dx_dtype, device=x.device)
+        self.dw = torch.empty(k, n, dtype=dw_dtype, device=x.device)
+        self._plan = ctypes.c_void_p()
+        check(_lib().sd_layer_plan_create(ctypes.byref(self._plan), x.data_ptr(), w.data_ptr(), dy.data_ptr(),
+                                          self.y.data_ptr(), _dtype_code(y_dtype), self.dx.data_ptr(),
+                                          _dtype_code(dx_dtype), self.dw.data_ptr(), _dtype_code(dw_dtype),
+                                          m, n, k, float(p), self.mask.cptr()))
+        self.scale = dropout_scale(p)
+
+    def forward(self, seed: int, stream=None):
+        check(_lib().sd_layer_plan_forward(self._plan, seed & MASK64, ctypes.c_void_p(_stream(stream))))
+        return self.y
+
+    def backward(self, stream=None):
+        check(_lib().sd_layer_plan_backward(self._plan, ctypes.c_void_p(_stream(stream))))
+        return self.dx, self.dw
+
+    def backward_dw(self, stream=None):
+        check(_lib().sd_layer_plan_backward_dw(self._plan, ctypes.c_void_p(_stream(stream))))
+        return self.dw
+
+    def backward_dx(self, stream=None):
+        check(_lib().sd_layer_plan_backward_dx(self._plan, ctypes.c_void_p(_stream(stream))))
+        return self.dx
+
+    def dense_forward(self, stream=None):
+        check(_lib().sd_layer_plan_dense_forward(self._plan, ctypes.c_void_p(_stream(stream))))
+        return self.y
+
+    def dense_backward(self, stream=None):
+        check(_lib().sd_layer_plan_dense_backward(self._plan, ctypes.c_void_p(_stream(stream))))
+        return self.dx, self.dw
+
+    def __del__(self):
+        try:
+            if self._plan:
+                _lib().sd_layer_plan_destroy(self._plan)
+                self._plan = ctypes.c_void_p()
+        except Exception:
+            pass
+
+
 def launch_count() -> int:
     """Kernels enqueued by libsparsedrop_b200.so in this process."""
     return int(_lib().sd_launch_count())

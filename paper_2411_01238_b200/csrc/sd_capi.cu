@@ -120,6 +120,8 @@ void check_col_blk(int blk, const char* which) {
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+uint64_t threshold_of(double p);
+uint64_t mix64_host(uint64_t z);
 
 GemmArgs base_args(int rows_out, int cols_out, int red, float scale, void* out) {
     GemmArgs a;
@@ -180,7 +182,10 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
         else
             cudaGetLastError();
     });
-    if (!g_encode) fail(SD_ERUNTIME, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    if (!g_encode) {
+        require_device();  // no device: report the missing B200 (there is no CPU fallback)
+        fail(SD_ERUNTIME, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    }
     CUtensorMap map;
     const cuuint64_t dims[2] = {inner, outer};
     const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
@@ -290,12 +295,7 @@ int sd_mask_sample(sd_block_mask* m, uint64_t seed, double p, int32_t rows, int3
                                 " blocks) does not match rows=" + str(rows) + " cols=" + str(cols));
         require_device();
         // keep iff (h >> 11) * 2^-53 >= p  <=>  (h >> 11) >= ceil(p * 2^53)  (exact: p*2^53 is exact)
-        const uint64_t threshold = static_cast<uint64_t>(std::ceil(std::ldexp(p, 53)));
-        uint64_t z = seed + 0x9E3779B97F4A7C15ull;
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-        z ^= z >> 31;
-        launch_mask_plan(*m, false, z, threshold, as_stream(stream));
+        launch_mask_plan(*m, false, mix64_host(seed), threshold_of(p), as_stream(stream));
     });
 }
 
@@ -335,47 +335,40 @@ int sd_mask_retile(const sd_block_mask* in, int32_t split_m, int32_t split_k, sd
 }
 
 // ---------------------------------------------------------------- GEMMs
+}  // extern "C"
 
-int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
-                  int32_t k, void* stream) {
-    return guarded([&] {
-        check_gemm(m, n, k);
-        check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
-        require_device();
-        GemmArgs g = base_args(m, n, k, 1.0f, c);
-        launch_gemm(false, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
-                    mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
-    });
+namespace sd {
+namespace {
+
+// A fully validated, ready-to-launch GEMM (tensor maps encoded).
+struct GemmCall {
+    bool a_mn = false, b_mn = false, f32 = false;
+    GemmKind kind = GemmKind::dsd;
+    CUtensorMap ta, tb, tout;
+    GemmArgs args;
+    void launch(cudaStream_t s) const { launch_gemm(a_mn, b_mn, kind, f32, ta, tb, tout, args, s); }
+};
+
+// dense c[m,n] = A * B with A (K-major | MN-major) and B (K-major | MN-major)
+GemmCall prep_dense(const void* a, bool a_mn, const void* b, bool b_mn, void* c, int c_dtype, int m, int n,
+                    int k) {
+    check_gemm(m, n, k);
+    check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
+    GemmCall g;
+    g.a_mn = a_mn;
+    g.b_mn = b_mn;
+    g.f32 = c_dtype == SD_DTYPE_F32;
+    g.kind = GemmKind::dsd;
+    g.ta = a_mn ? mnmajor_map(a, m, k) : kmajor_map(a, k, m);
+    g.tb = b_mn ? mnmajor_map(b, n, k) : kmajor_map(b, k, n);
+    g.tout = out_map(c, c_dtype, m, n);
+    g.args = base_args(m, n, k, 1.0f, c);
+    return g;
 }
 
-int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, int32_t m, int32_t n,
-                     int32_t k, void* stream) {
-    return guarded([&] {
-        check_gemm(m, n, k);
-        check_ptr(a, "a"), check_ptr(b_t, "b_t"), check_ptr(c, "c"), check_dtype(c_dtype);
-        require_device();
-        GemmArgs g = base_args(m, n, k, 1.0f, c);
-        launch_gemm(false, false, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
-                    kmajor_map(b_t, k, n), out_map(c, c_dtype, m, n), g, as_stream(stream));
-    });
-}
-
-int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
-                     int32_t k, void* stream) {
-    return guarded([&] {
-        check_gemm(m, n, k);
-        check_ptr(a_t, "a_t"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
-        require_device();
-        GemmArgs g = base_args(m, n, k, 1.0f, c);
-        launch_gemm(true, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, mnmajor_map(a_t, m, k),
-                    mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
-    });
-}
-
-// gemm.hpp:133-170 / layer.hpp:115
-static void dsd_forward(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
-                        int c_dtype, int m, int n, int k, unsigned long long* counters, void* stream,
-                        const char* where) {
+// gemm.hpp:133-170 / layer.hpp:115: c = s (a (.) m) b, skipping dropped K-blocks.
+GemmCall prep_dsd_forward(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
+                          int c_dtype, int m, int n, int k, unsigned long long* counters, const char* where) {
     check_gemm(m, n, k);
     check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
     if (!mask) fail(SD_EINVAL, std::string(where) + ": null mask");
@@ -384,35 +377,29 @@ static void dsd_forward(const void* a, const sd_block_mask* mask, const void* b,
     check_mask_geometry(mask, m / mask->m_blk, k / mask->k_blk, mask->m_blk, mask->k_blk, where);
     check_row_blk(mask->m_blk, "m_blk");
     check_red_blk(mask->k_blk, "k_blk");
-    require_device();
-    GemmArgs g = base_args(m, n, k, scale, c);
-    g.list_cnt = mask->row_cnt;
-    g.list_idx = mask->row_idx;
-    g.list_stride = mask->block_cols;
-    g.red_blk = mask->k_blk;
-    g.out_row_blk = mask->m_blk;
-    g.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
-    g.counters = counters;
-    launch_gemm(false, true, GemmKind::dsd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m),
-                mnmajor_map(b, n, k), out_map(c, c_dtype, m, n), g, as_stream(stream));
+    GemmCall g;
+    g.a_mn = false;
+    g.b_mn = true;
+    g.f32 = c_dtype == SD_DTYPE_F32;
+    g.kind = GemmKind::dsd;
+    g.ta = kmajor_map(a, k, m);
+    g.tb = mnmajor_map(b, n, k);
+    g.tout = out_map(c, c_dtype, m, n);
+    g.args = base_args(m, n, k, scale, c);
+    g.args.list_cnt = mask->row_cnt;
+    g.args.list_idx = mask->row_idx;
+    g.args.list_stride = mask->block_cols;
+    g.args.red_blk = mask->k_blk;
+    g.args.out_row_blk = mask->m_blk;
+    g.args.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
+    g.args.counters = counters;
+    return g;
 }
 
-int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
-                  int32_t c_dtype, int32_t m, int32_t n, int32_t k, unsigned long long* counters,
-                  void* stream) {
-    return guarded([&] { dsd_forward(a, mask, b, scale, c, c_dtype, m, n, k, counters, stream, "dsd_matmul"); });
-}
-
-int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
-                      int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
-    return guarded(
-        [&] { dsd_forward(x, mask, w, scale, y, y_dtype, m, n, k, nullptr, stream, "layer forward"); });
-}
-
-// gemm.hpp:176-213. b_kmajor: b is given as b^T (n x k row-major), i.e. the layer's W.
-static void sdd(const void* a, const void* b, bool b_kmajor, const sd_block_mask* mask, float scale,
-                void* c, int c_dtype, int m, int n, int k, unsigned long long* counters, void* stream,
-                const char* where) {
+// gemm.hpp:176-213: c[m,n] = s (a[m,k] b[k,n]) on kept output blocks. b_kmajor: b is
+// supplied as b^T (n x k row-major), e.g. the layer's W for dX (layer.hpp:158).
+GemmCall prep_sdd(const void* a, const void* b, bool b_kmajor, const sd_block_mask* mask, float scale,
+                  void* c, int c_dtype, int m, int n, int k, unsigned long long* counters, const char* where) {
     check_gemm(m, n, k);
     check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
     if (!mask) fail(SD_EINVAL, std::string(where) + ": null mask");
@@ -421,59 +408,237 @@ static void sdd(const void* a, const void* b, bool b_kmajor, const sd_block_mask
     check_mask_geometry(mask, m / mask->m_blk, n / mask->k_blk, mask->m_blk, mask->k_blk, where);
     check_row_blk(mask->m_blk, "m_blk");
     check_col_blk(mask->k_blk, "n_blk");
-    require_device();
-    GemmArgs g = base_args(m, n, k, scale, c);
-    g.words = mask->words;
-    g.mask_cols = mask->block_cols;
-    g.out_col_blk = mask->k_blk;
-    g.out_row_blk = mask->m_blk;
-    g.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
-    g.counters = counters;
-    const CUtensorMap tb = b_kmajor ? kmajor_map(b, k, n) : mnmajor_map(b, n, k);
-    launch_gemm(false, !b_kmajor, GemmKind::sdd, c_dtype == SD_DTYPE_F32, kmajor_map(a, k, m), tb,
-                out_map(c, c_dtype, m, n), g, as_stream(stream));
+    GemmCall g;
+    g.a_mn = false;
+    g.b_mn = !b_kmajor;
+    g.f32 = c_dtype == SD_DTYPE_F32;
+    g.kind = GemmKind::sdd;
+    g.ta = kmajor_map(a, k, m);
+    g.tb = b_kmajor ? kmajor_map(b, k, n) : mnmajor_map(b, n, k);
+    g.tout = out_map(c, c_dtype, m, n);
+    g.args = base_args(m, n, k, scale, c);
+    g.args.words = mask->words;
+    g.args.mask_cols = mask->block_cols;
+    g.args.out_col_blk = mask->k_blk;
+    g.args.out_row_blk = mask->m_blk;
+    g.args.row_order = mask->m_blk == kBM ? mask->row_order : nullptr;
+    g.args.counters = counters;
+    return g;
+}
+
+// layer.hpp:158: dx (m x k) = s (dy (m x n) W^T) (.) m — the sdd problem (M, K_out=k, N_red=n).
+GemmCall prep_layer_dx(const void* dy, const void* w, const sd_block_mask* mask, float scale, void* dx,
+                       int dx_dtype, int m, int n, int k) {
+    return prep_sdd(dy, w, true, mask, scale, dx, dx_dtype, m, k, n, nullptr, "layer backward dx");
+}
+
+// layer.hpp:159-160: dw (k x n) = s (x (.) m)^T dy over the mask's column lists —
+// the dsd problem (K_out = k rows, N, M_red = m) with x read MN-major in place.
+GemmCall prep_layer_dw(const void* x, const sd_block_mask* mask, const void* dy, float scale, void* dw,
+                       int dw_dtype, int m, int n, int k) {
+    check_gemm(k, n, m);
+    check_ptr(x, "x"), check_ptr(dy, "dy"), check_ptr(dw, "dw"), check_dtype(dw_dtype);
+    if (!mask) fail(SD_EINVAL, "layer backward dw: null mask");
+    check_divides(mask->m_blk, m, "m_blk");
+    check_divides(mask->k_blk, k, "k_blk");
+    check_mask_geometry(mask, m / mask->m_blk, k / mask->k_blk, mask->m_blk, mask->k_blk, "layer backward dw");
+    check_row_blk(mask->k_blk, "k_blk");
+    check_red_blk(mask->m_blk, "m_blk");
+    GemmCall g;
+    g.a_mn = true;
+    g.b_mn = true;
+    g.f32 = dw_dtype == SD_DTYPE_F32;
+    g.kind = GemmKind::dsd;
+    g.ta = mnmajor_map(x, k, m);
+    g.tb = mnmajor_map(dy, n, m);
+    g.tout = out_map(dw, dw_dtype, k, n);
+    g.args = base_args(k, n, m, scale, dw);
+    g.args.list_cnt = mask->col_cnt;
+    g.args.list_idx = mask->col_idx;
+    g.args.list_stride = mask->block_rows;
+    g.args.red_blk = mask->m_blk;
+    g.args.out_row_blk = mask->k_blk;
+    g.args.row_order = mask->k_blk == kBM ? mask->col_order : nullptr;
+    return g;
+}
+
+uint64_t threshold_of(double p) { return static_cast<uint64_t>(std::ceil(std::ldexp(p, 53))); }
+
+uint64_t mix64_host(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+float dropout_scale_f32(double p) { return static_cast<float>(1.0 / (1.0 - p)); }
+
+}  // namespace
+}  // namespace sd
+
+struct sd_layer_plan {
+    sd_block_mask mask;
+    double p;
+    uint64_t threshold;
+    int device;
+    sd::GemmCall fwd, dw, dx, dense_fwd, dense_dw, dense_dx;
+};
+
+extern "C" {
+
+int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n, int32_t k,
+                  void* stream) {
+    return guarded([&] {
+        auto g = prep_dense(a, false, b, true, c, c_dtype, m, n, k);
+        require_device();
+        g.launch(as_stream(stream));
+    });
+}
+
+int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                     int32_t k, void* stream) {
+    return guarded([&] {
+        auto g = prep_dense(a, false, b_t, false, c, c_dtype, m, n, k);
+        require_device();
+        g.launch(as_stream(stream));
+    });
+}
+
+int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n,
+                     int32_t k, void* stream) {
+    return guarded([&] {
+        auto g = prep_dense(a_t, true, b, true, c, c_dtype, m, n, k);
+        require_device();
+        g.launch(as_stream(stream));
+    });
+}
+
+int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float scale, void* c,
+                  int32_t c_dtype, int32_t m, int32_t n, int32_t k, unsigned long long* counters,
+                  void* stream) {
+    return guarded([&] {
+        auto g = prep_dsd_forward(a, mask, b, scale, c, c_dtype, m, n, k, counters, "dsd_matmul");
+        require_device();
+        g.launch(as_stream(stream));
+    });
+}
+
+int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
+                      int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
+    return guarded([&] {
+        auto g = prep_dsd_forward(x, mask, w, scale, y, y_dtype, m, n, k, nullptr, "layer forward");
+        require_device();
+        g.launch(as_stream(stream));
+    });
 }
 
 int sd_sdd_matmul(const void* a, const void* b, const sd_block_mask* mask, float scale, void* c,
                   int32_t c_dtype, int32_t m, int32_t n, int32_t k, unsigned long long* counters,
                   void* stream) {
-    return guarded([&] { sdd(a, b, false, mask, scale, c, c_dtype, m, n, k, counters, stream, "sdd_matmul"); });
+    return guarded([&] {
+        auto g = prep_sdd(a, b, false, mask, scale, c, c_dtype, m, n, k, counters, "sdd_matmul");
+        require_device();
+        g.launch(as_stream(stream));
+    });
 }
 
-// layer.hpp:158: dx (m x k) = s * (dy (m x n) * W^T) (.) m, W (k x n) read in place.
 int sd_linear_backward_dx(const void* dy, const void* w, const sd_block_mask* mask, float scale, void* dx,
                           int32_t dx_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
     return guarded([&] {
-        // the sdd problem is (M, K_out = k, N_red = n)
-        sdd(dy, w, true, mask, scale, dx, dx_dtype, m, k, n, nullptr, stream, "layer backward dx");
+        auto g = prep_layer_dx(dy, w, mask, scale, dx, dx_dtype, m, n, k);
+        require_device();
+        g.launch(as_stream(stream));
     });
 }
 
-// layer.hpp:159-160: dw (k x n) = s * (x (.) m)^T dy over the column lists of m.
 int sd_linear_backward_dw(const void* x, const sd_block_mask* mask, const void* dy, float scale, void* dw,
                           int32_t dw_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
     return guarded([&] {
-        // the dsd problem is (K_out = k rows, N, M_red = m)
-        check_gemm(k, n, m);
-        check_ptr(x, "x"), check_ptr(dy, "dy"), check_ptr(dw, "dw"), check_dtype(dw_dtype);
-        if (!mask) fail(SD_EINVAL, "layer backward dw: null mask");
-        check_divides(mask->m_blk, m, "m_blk");
-        check_divides(mask->k_blk, k, "k_blk");
-        check_mask_geometry(mask, m / mask->m_blk, k / mask->k_blk, mask->m_blk, mask->k_blk,
-                            "layer backward dw");
-        check_row_blk(mask->k_blk, "k_blk");
-        check_red_blk(mask->m_blk, "m_blk");
+        auto g = prep_layer_dw(x, mask, dy, scale, dw, dw_dtype, m, n, k);
         require_device();
-        GemmArgs g = base_args(k, n, m, scale, dw);
-        g.list_cnt = mask->col_cnt;
-        g.list_idx = mask->col_idx;
-        g.list_stride = mask->block_rows;
-        g.red_blk = mask->m_blk;
-        g.out_row_blk = mask->k_blk;
-        g.row_order = mask->k_blk == kBM ? mask->col_order : nullptr;
-        launch_gemm(true, true, GemmKind::dsd, dw_dtype == SD_DTYPE_F32, mnmajor_map(x, k, m),
-                    mnmajor_map(dy, n, m), out_map(dw, dw_dtype, k, n), g, as_stream(stream));
+        g.launch(as_stream(stream));
     });
+}
+
+// ---------------------------------------------------------------- layer plan
+
+int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, const void* dy, void* y,
+                         int32_t y_dtype, void* dx, int32_t dx_dtype, void* dw, int32_t dw_dtype, int32_t m,
+                         int32_t n, int32_t k, double p, const sd_block_mask* mask) {
+    return guarded([&] {
+        if (!out) fail(SD_EINVAL, "sd_layer_plan_create: null plan pointer");
+        *out = nullptr;
+        if (!(p >= 0.0 && p < 1.0)) {
+            char buf[64];
+            std::snprintf(buf, sizeof buf, "%f", p);
+            fail(SD_EINVAL, std::string("dropout rate must lie in [0, 1), got ") + buf);
+        }
+        if (!mask) fail(SD_EINVAL, "sd_layer_plan_create: null mask");
+        const float s = dropout_scale_f32(p);
+        sd_layer_plan tmp;
+        tmp.mask = *mask;
+        tmp.p = p;
+        tmp.threshold = threshold_of(p);
+        tmp.fwd = prep_dsd_forward(x, mask, w, s, y, y_dtype, m, n, k, nullptr, "layer forward");
+        tmp.dw = prep_layer_dw(x, mask, dy, s, dw, dw_dtype, m, n, k);
+        tmp.dx = prep_layer_dx(dy, w, mask, s, dx, dx_dtype, m, n, k);
+        require_device();
+        cudaGetDevice(&tmp.device);
+        tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
+        tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
+        tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
+        *out = new sd_layer_plan(tmp);
+    });
+}
+
+int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, as_stream(stream));
+        plan->fwd.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        plan->dw.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        plan->dx.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        plan->dw.launch(as_stream(stream));
+        plan->dx.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        plan->dense_fwd.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        plan->dense_dw.launch(as_stream(stream));
+        plan->dense_dx.launch(as_stream(stream));
+    });
+}
+
+int sd_layer_plan_destroy(sd_layer_plan* plan) {
+    delete plan;
+    return SD_OK;
 }
 
 uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k) { return 2ull * m * n * k; }
