@@ -418,6 +418,9 @@ GemmCall prep_sdd(const void* a, const void* b, bool b_kmajor, const sd_block_ma
     g.tout = out_map(c, c_dtype, m, n);
     g.args = base_args(m, n, k, scale, c);
     g.args.words = mask->words;
+    g.args.list_cnt = mask->row_cnt;
+    g.args.list_idx = mask->row_idx;
+    g.args.list_stride = mask->block_cols;
     g.args.mask_cols = mask->block_cols;
     g.args.out_col_blk = mask->k_blk;
     g.args.out_row_blk = mask->m_blk;

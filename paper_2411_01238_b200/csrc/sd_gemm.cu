@@ -8,7 +8,8 @@
 //     dW       dW = s (X (.) m)^T dY   A = X  MN-major, B = dY MN-major, column lists
 //     dense    (list == null: every reduction block)
 //   sdd (output-block skipping, gemm.hpp:176-213):
-//     dX       dX = s (dY W^T) (.) m   A = dY K-major, B = W  K-major, mask bits
+//     dX       dX = s (dY W^T) (.) m   A = dY K-major, B = W  K-major, row lists
+//              (kept output blocks packed two per 256-wide unit; dropped = +0.0)
 //
 // Tile: 128 output rows (one tcgen05 M=128 MMA, TMEM lanes = rows) x up to 256
 // output columns (MMA N chosen per tile at run time: 256, or 128 for a ragged
@@ -83,17 +84,19 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
         t.nstages = cnt * (a.red_blk / kBK);
         if (cnt == 0) t.n_eff = 0;
     } else {
+        // Pack the row's KEPT output blocks (compacted list, ascending) into
+        // 256-wide units, so every unit but the row's last runs a full N=256 MMA;
+        // the same unit index also zero-fills the row's DROPPED blocks (kept at
+        // the tail of the list by the mask kernel).
         const int per_unit = kBN / a.out_col_blk;
-        const int b0 = cu * per_unit;
-        const int nb = min(per_unit, a.mask_cols - b0);
-        t.n0 = b0 * a.out_col_blk;
-        for (int j = 0; j < nb; ++j) {
-            const int64_t b = static_cast<int64_t>(t.list_row) * a.mask_cols + b0 + j;
-            const bool kept = (__ldg(a.words + (b >> 6)) >> (b & 63)) & 1ull;
-            if (kept)
-                t.slot_blk[t.nslots++] = b0 + j;
-            else
-                t.zero_blk[t.nzero++] = b0 + j;
+        const int cnt = __ldg(a.list_cnt + t.list_row);
+        const int ndrop = a.mask_cols - cnt;
+        const int32_t* row = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride;
+        t.n0 = 0;
+        for (int j = 0; j < per_unit; ++j) {
+            const int li = cu * per_unit + j;
+            if (li < cnt) t.slot_blk[t.nslots++] = __ldg(row + li);
+            if (li < ndrop) t.zero_blk[t.nzero++] = __ldg(row + a.mask_cols - 1 - li);
         }
         t.n_eff = t.nslots * a.out_col_blk;
         t.nstages = a.red / kBK;

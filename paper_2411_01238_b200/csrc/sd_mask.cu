@@ -8,8 +8,9 @@
 //     r0 + r and is bit-identical to the matching rows of the global mask.
 // K2 (kept_blocks_in_row, block_mask.cpp:125-135, on the mask and on
 //     transpose_mask, :117-123): warp-ballot compaction, one warp per block row
-//     (row lists) and one warp per block column (column lists); positions are
-//     the popcount of the ballot below the lane, so lists come out strictly
+//     (row lists; the dropped columns fill the row's tail for the sdd zero
+//     fill) and one block per block column (column lists); positions are the
+//     popcount of the ballot below the lane, so lists come out strictly
 //     increasing like the reference's.
 // The three parts read nothing but (seed, r, c) — each recomputes the hash — so
 // they run as independent blocks of a single grid; the last block to finish
@@ -126,54 +127,72 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     int blk = blockIdx.x;
 
     if (blk < a.nb_words) {
-        // ---- words: one thread per 64-bit word (hash mode only)
+        // ---- words: one warp per 64-bit word, two bits per lane, ballot-packed
         const int64_t total = static_cast<int64_t>(R) * C;
         const int64_t nwords = (total + 63) / 64;
-        const int64_t w = static_cast<int64_t>(blk) * kThreads + threadIdx.x;
+        const int64_t w = static_cast<int64_t>(blk) * (kThreads / 32) + wid;
         if (w < nwords) {
-            int64_t b = w * 64;
-            int r = static_cast<int>(b / C), c = static_cast<int>(b % C);
-            uint64_t word = 0;
-            for (int i = 0; i < 64 && b < total; ++i, ++b) {
-                word |= static_cast<uint64_t>(keep_bit(a, r, c)) << i;
-                if (++c == C) {
-                    c = 0;
-                    ++r;
-                }
-            }
-            a.m.words[w] = word;
+            const int64_t b0 = w * 64 + lane, b1 = b0 + 32;
+            const bool k0 = b0 < total && keep_bit(a, static_cast<int>(b0 / C), static_cast<int>(b0 % C));
+            const bool k1 = b1 < total && keep_bit(a, static_cast<int>(b1 / C), static_cast<int>(b1 % C));
+            const uint32_t lo = __ballot_sync(0xffffffffu, k0);
+            const uint32_t hi = __ballot_sync(0xffffffffu, k1);
+            if (lane == 0) a.m.words[w] = (static_cast<uint64_t>(hi) << 32) | lo;
         }
     } else if ((blk -= a.nb_words) < a.nb_rows) {
-        // ---- row lists: one warp per block row
+        // ---- row lists: one warp per block row. Kept columns ascending from the
+        // front (kept_blocks_in_row), dropped columns from the back (the sdd
+        // kernel's zero-fill list).
         const int r = blk * (kThreads / 32) + wid;
         if (r < R) {
-            int base = 0;
+            int base = 0, dbase = 0;
             int32_t* dst = a.m.row_idx + static_cast<int64_t>(r) * C;
             for (int c0 = 0; c0 < C; c0 += 32) {
                 const int c = c0 + lane;
-                const bool k = c < C && keep_bit(a, r, c);
+                const bool valid = c < C;
+                const bool k = valid && keep_bit(a, r, c);
                 const uint32_t bal = __ballot_sync(0xffffffffu, k);
+                const uint32_t dbal = __ballot_sync(0xffffffffu, valid && !k);
                 if (k) dst[base + __popc(bal & lt)] = c;
+                if (valid && !k) dst[C - 1 - (dbase + __popc(dbal & lt))] = c;
                 base += __popc(bal);
+                dbase += __popc(dbal);
             }
             if (lane == 0) a.m.row_cnt[r] = base;
         }
     } else {
-        // ---- column lists: one warp per block column
-        blk -= a.nb_rows;
-        const int c = blk * (kThreads / 32) + wid;
-        if (c < C) {
-            int base = 0;
-            int32_t* dst = a.m.col_idx + static_cast<int64_t>(c) * R;
-            for (int r0 = 0; r0 < R; r0 += 32) {
-                const int r = r0 + lane;
-                const bool k = r < R && keep_bit(a, r, c);
-                const uint32_t bal = __ballot_sync(0xffffffffu, k);
-                if (k) dst[base + __popc(bal & lt)] = r;
-                base += __popc(bal);
-            }
-            if (lane == 0) a.m.col_cnt[c] = base;
+        // ---- column lists: one block per block column; warps take contiguous
+        // 32-row chunks, ballots parked in smem, block scan, then scatter.
+        const int c = blk - a.nb_rows;
+        uint32_t* bal_s = reinterpret_cast<uint32_t*>(dyn_smem);
+        const int nchunks = (R + 31) / 32;
+        const int per_warp = (nchunks + kThreads / 32 - 1) / (kThreads / 32);
+        const int ch0 = wid * per_warp;
+        const int ch1 = min(nchunks, ch0 + per_warp);
+        int cnt = 0;
+        for (int ch = ch0; ch < ch1; ++ch) {
+            const int r = ch * 32 + lane;
+            const bool k = r < R && keep_bit(a, r, c);
+            const uint32_t bal = __ballot_sync(0xffffffffu, k);
+            if (lane == 0) bal_s[ch] = bal;
+            cnt += __popc(bal);
         }
+        if (lane == 0) warp_tot[wid] = cnt;
+        __syncthreads();
+        int base = 0;
+        for (int i = 0; i < wid; ++i) base += warp_tot[i];
+        int32_t* dst = a.m.col_idx + static_cast<int64_t>(c) * R;
+        for (int ch = ch0; ch < ch1; ++ch) {
+            const uint32_t bal = bal_s[ch];
+            if ((bal >> lane) & 1u) dst[base + __popc(bal & lt)] = ch * 32 + lane;
+            base += __popc(bal);
+        }
+        if (threadIdx.x == kThreads - 1) {
+            int tot = 0;
+            for (int i = 0; i < kThreads / 32; ++i) tot += warp_tot[i];
+            a.m.col_cnt[c] = tot;
+        }
+        __syncthreads();
     }
 
     // ---- last block: keep_count and cost orders
@@ -245,12 +264,21 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     a.seed_mix = seed_mix;
     a.threshold = threshold;
     const int64_t nwords = (static_cast<int64_t>(m.block_rows) * m.block_cols + 63) / 64;
-    a.nb_words = from_words ? 0 : static_cast<int>((nwords + kThreads - 1) / kThreads);
+    a.nb_words = from_words ? 0 : static_cast<int>((nwords + kThreads / 32 - 1) / (kThreads / 32));
     a.nb_rows = (m.block_rows + kThreads / 32 - 1) / (kThreads / 32);
-    a.nb_cols = (m.block_cols + kThreads / 32 - 1) / (kThreads / 32);
+    a.nb_cols = m.block_cols;
     const int grid = a.nb_words + a.nb_rows + a.nb_cols;
     const int bins = std::min(std::max(m.block_rows, m.block_cols) + 1, kMaxOrderBins);
-    const size_t smem = static_cast<size_t>(bins) * sizeof(int);
+    const int chunks = (m.block_rows + 31) / 32;
+    const size_t smem = static_cast<size_t>(std::max(bins, chunks)) * sizeof(int);
+    if (smem > 48 * 1024) {
+        static bool raised = false;
+        if (!raised) {
+            check_cuda(cudaFuncSetAttribute(mask_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                       "mask_plan_kernel smem");
+            raised = true;
+        }
+    }
     mask_plan_kernel<<<grid, kThreads, smem, s>>>(a);
     check_cuda(cudaGetLastError(), "mask_plan_kernel launch");
     note_launch();
