@@ -436,6 +436,39 @@ def main():
             if p != args.p:
                 plans.pop(p, None)
 
+    # ---- T8: the north-star 8192^3 target (sparse p=0.1/0.5 vs our dense), single GPU only
+    t8 = None
+    if world == 1 and not args.no_sweep and S != 8192:
+        S8 = 8192
+        x8, w8, dy8 = synth(S8, S8), synth(S8, S8), synth(S8, S8)
+        t8 = {"shape": [S8, S8, S8]}
+        for p8 in (0.0, 0.1, 0.5):
+            pl8 = sd.LayerPlan(x8, w8, dy8, p8)
+
+            def st8(i, pl8=pl8):
+                pl8.forward(seed=sd.effective_seed(0, i, 0))
+                pl8.backward()
+
+            ms8 = time_steps(st8, max(5, args.steps // 2), 3)
+            k8 = pl8.mask.keep_count() / pl8.mask.total_blocks()
+            t8[f"p{p8}"] = {"ms_per_step": ms8, "keep": k8,
+                            "dense_equiv_tflops": 3 * 2 * S8 ** 3 / (ms8 * 1e-3) / 1e12,
+                            "executed_tflops": k8 * 3 * 2 * S8 ** 3 / (ms8 * 1e-3) / 1e12}
+            if p8 == 0.5:
+                def dn8(i, pl8=pl8):
+                    pl8.dense_forward()
+                    pl8.dense_backward()
+
+                msd8 = time_steps(dn8, max(5, args.steps // 2), 3)
+                t8["dense_ms_per_step"] = msd8
+                t8["dense_tflops"] = 3 * 2 * S8 ** 3 / (msd8 * 1e-3) / 1e12
+                t8["speedup_vs_dense_p0.5"] = msd8 / ms8
+            del pl8
+        mst = time_steps(lambda i: (x8 @ w8, x8.t() @ dy8, dy8 @ w8.t()), max(5, args.steps // 2), 3)
+        t8["torch_cublas_dense_tflops"] = 3 * 2 * S8 ** 3 / (mst * 1e-3) / 1e12
+        del x8, w8, dy8
+        torch.cuda.empty_cache()
+
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -485,6 +518,7 @@ def main():
             "gpu_launches": gpu_launches,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "sweep": sweep,
+            "t8": t8,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -171,6 +171,27 @@ int num_sms() {
 
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+unsigned int* sched_slot() {
+    constexpr int kSlots = 256;
+    static unsigned int* slots[64] = {nullptr};
+    static std::atomic<uint32_t> next{0};
+    static std::mutex mu;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) fail(SD_ERUNTIME, "device index out of range");
+    if (!slots[dev]) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!slots[dev]) {
+            unsigned int* p = nullptr;
+            check_cuda(cudaMalloc(&p, kSlots * 2 * sizeof(unsigned int)), "cudaMalloc(scheduler slots)");
+            check_cuda(cudaMemset(p, 0, kSlots * 2 * sizeof(unsigned int)), "cudaMemset(scheduler slots)");
+            check_cuda(cudaDeviceSynchronize(), "scheduler slots init");
+            slots[dev] = p;
+        }
+    }
+    return slots[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
+}
+
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
                          uint32_t box_outer) {
     std::call_once(g_encode_once, [] {
@@ -587,6 +608,7 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dx = prep_layer_dx(dy, w, mask, s, dx, dx_dtype, m, n, k);
         require_device();
         cudaGetDevice(&tmp.device);
+        (void)sched_slot();  // allocate the scheduler slots now (keeps launches capturable)
         tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);

@@ -48,9 +48,11 @@ constexpr int kOffA = 0;
 constexpr int kOffB = kOffA + kStages * kABytes;
 constexpr int kOffEpi = kOffB + kStages * kBBytes;
 constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
-constexpr int kNumBars = 2 * kStages + 4;
+constexpr int kSchedDepth = 4;  // unit-index ring between the producer and the consumers
+constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth;
 constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
-constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
+constexpr int kOffSched = kOffTmemSlot + 16;
+constexpr int kSmemBytes = kOffSched + 4 * kSchedDepth + 1024;  // + alignment slack
 
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
@@ -69,8 +71,18 @@ struct Unit {
 template <bool SDD>
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
     Unit t;
-    const int i = u / a.n_col_units;
-    const int cu = u - i * a.n_col_units;
+    // dsd: row-major over (tile row, column unit), tile rows heaviest first.
+    // sdd: column-unit-major, so the units that carry MMA work (low unit index
+    //      within a row: kept blocks are packed first) are handed out first and
+    //      the zero-fill-only units last.
+    int i, cu;
+    if constexpr (!SDD) {
+        i = u / a.n_col_units;
+        cu = u - i * a.n_col_units;
+    } else {
+        cu = u / a.n_row_tiles;
+        i = u - cu * a.n_row_tiles;
+    }
     const int rt = a.row_order ? __ldg(a.row_order + i) : i;
     t.row0 = rt * kBM;
     t.list_row = t.row0 / a.out_row_blk;
@@ -134,7 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty_bar = bars + kStages;
     uint64_t* tfull_bar = bars + 2 * kStages;
     uint64_t* tempty_bar = bars + 2 * kStages + 2;
+    uint64_t* sfull_bar = bars + 2 * kStages + 4;
+    uint64_t* sempty_bar = sfull_bar + kSchedDepth;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+    volatile int* sched_unit = reinterpret_cast<volatile int*>(smem + kOffSched);
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
@@ -152,6 +167,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(tfull_bar + i, 1);
             ptx::mbar_init(tempty_bar + i, kEpiWarps);
         }
+        for (int i = 0; i < kSchedDepth; ++i) {
+            ptx::mbar_init(sfull_bar + i, 1);
+            ptx::mbar_init(sempty_bar + i, 1 + kEpiWarps);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -166,8 +185,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol = ptx::policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            int sslot = 0;
+            uint32_t sphase = 0;
+            // Dynamic persistent scheduling: first unit = blockIdx.x, then work
+            // stealing through a global atomic counter (units are ordered
+            // heaviest first, so this is greedy longest-processing-time).
+            int u = blockIdx.x;
+            while (true) {
+                ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1);
+                sched_unit[sslot] = u;
+                ptx::mbar_arrive(sfull_bar + sslot);
+                if (++sslot == kSchedDepth) {
+                    sslot = 0;
+                    sphase ^= 1;
+                }
+                if (u >= num_units) break;
+                const int next = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u));
                 const Unit t = decode_unit<SDD>(args, u);
+                u = next;
                 if (t.n_eff == 0) continue;
                 const uint32_t tx_bytes = kABytes + t.n_eff * kBK * 2;
                 const int spb = args.red_blk / kBK;
@@ -231,7 +266,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_iter = 0;
-            for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+            int sslot = 0;
+            uint32_t sphase = 0;
+            while (true) {
+                ptx::mbar_wait(sfull_bar + sslot, sphase);
+                const int u = sched_unit[sslot];
+                ptx::mbar_arrive(sempty_bar + sslot);
+                if (++sslot == kSchedDepth) {
+                    sslot = 0;
+                    sphase ^= 1;
+                }
+                if (u >= num_units) break;
                 const Unit t = decode_unit<SDD>(args, u);
                 if (t.n_eff == 0) continue;
                 const uint32_t acc = acc_iter & 1;
@@ -274,7 +319,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t bi = 0;
         uint32_t acc_iter = 0;
         constexpr int kChunkCols = OUT_F32 ? 32 : 64;  // 128 bytes of output per row
-        for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int sslot = 0;
+        uint32_t sphase = 0;
+        while (true) {
+            ptx::mbar_wait(sfull_bar + sslot, sphase);
+            const int u = sched_unit[sslot];
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(sempty_bar + sslot);
+            if (++sslot == kSchedDepth) {
+                sslot = 0;
+                sphase ^= 1;
+            }
+            if (u >= num_units) break;
             const Unit t = decode_unit<SDD>(args, u);
             const int row_first = t.row0 + 32 * q;
             if constexpr (SDD) {
@@ -352,6 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    if (threadIdx.x == 0) {
+        // last CTA out re-arms the scheduler slot for the next launch
+        __threadfence();
+        if (atomicAdd(args.sched + 1, 1u) == gridDim.x - 1) {
+            args.sched[0] = 0u;
+            args.sched[1] = 0u;
+            __threadfence();
+        }
+    }
 }
 
 template <bool A_MN, bool B_MN, bool SDD, bool OUT_F32>
@@ -367,7 +432,9 @@ void launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
     const int units = args.n_row_tiles * args.n_col_units;
     const int grid = units < num_sms() ? units : num_sms();
     if (grid <= 0) return;
-    kern<<<grid, kThreads, kSmemBytes, s>>>(ta, tb, tout, args);
+    GemmArgs a = args;
+    a.sched = sched_slot();
+    kern<<<grid, kThreads, kSmemBytes, s>>>(ta, tb, tout, a);
     check_cuda(cudaGetLastError(), "sd_gemm_kernel launch");
     note_launch();
 }

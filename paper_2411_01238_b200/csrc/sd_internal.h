@@ -56,7 +56,12 @@ struct GemmArgs {
     float scale;
     void* out;
     unsigned long long* counters;
+    unsigned int* sched;  // {next-unit counter, CTAs-done counter}, zero between launches
 };
+
+// A zeroed {counter, done} pair for one persistent-kernel launch (ring of
+// slots per device, re-armed by the last CTA of the launch that used it).
+unsigned int* sched_slot();
 
 // A_MN / B_MN: operand is MN-major (contiguous along the output dimension)
 // rather than K-major (contiguous along the reduction).
