@@ -506,7 +506,24 @@ struct sd_layer_plan {
     uint64_t threshold;
     int device;
     sd::GemmCall fwd, dw, dx, dense_fwd, dense_dw, dense_dx;
+    // backward fork/join: dX runs on `aux` concurrently with dW on the caller's
+    // stream, so each persistent kernel's CTAs fill the other's tail
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
+
+namespace {
+// Enqueue `first` on s and `second` on the plan's auxiliary stream, both after
+// everything already on s; s waits for both.
+void fork_join(sd_layer_plan* plan, const sd::GemmCall& first, const sd::GemmCall& second, cudaStream_t s) {
+    sd::check_cuda(cudaEventRecord(plan->fork, s), "cudaEventRecord(fork)");
+    sd::check_cuda(cudaStreamWaitEvent(plan->aux, plan->fork, 0), "cudaStreamWaitEvent(aux)");
+    second.launch(plan->aux);
+    first.launch(s);
+    sd::check_cuda(cudaEventRecord(plan->join, plan->aux), "cudaEventRecord(join)");
+    sd::check_cuda(cudaStreamWaitEvent(s, plan->join, 0), "cudaStreamWaitEvent(join)");
+}
+}  // namespace
 
 extern "C" {
 
@@ -612,6 +629,9 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
+        check_cuda(cudaStreamCreateWithFlags(&tmp.aux, cudaStreamNonBlocking), "cudaStreamCreate(aux)");
+        check_cuda(cudaEventCreateWithFlags(&tmp.fork, cudaEventDisableTiming), "cudaEventCreate");
+        check_cuda(cudaEventCreateWithFlags(&tmp.join, cudaEventDisableTiming), "cudaEventCreate");
         *out = new sd_layer_plan(tmp);
     });
 }
@@ -641,8 +661,9 @@ int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
 int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        plan->dw.launch(as_stream(stream));
-        plan->dx.launch(as_stream(stream));
+        // dX (coarse units: full-N reductions) starts first on the aux stream;
+        // dW's finer units fill its tail.
+        fork_join(plan, plan->dw, plan->dx, as_stream(stream));
     });
 }
 
@@ -656,12 +677,16 @@ int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream) {
 int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        plan->dense_dw.launch(as_stream(stream));
-        plan->dense_dx.launch(as_stream(stream));
+        fork_join(plan, plan->dense_dw, plan->dense_dx, as_stream(stream));
     });
 }
 
 int sd_layer_plan_destroy(sd_layer_plan* plan) {
+    if (plan) {
+        if (plan->aux) cudaStreamDestroy(plan->aux);
+        if (plan->fork) cudaEventDestroy(plan->fork);
+        if (plan->join) cudaEventDestroy(plan->join);
+    }
     delete plan;
     return SD_OK;
 }

@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Everything above overlapped the previous kernel's tail (PDL); from here on
+    // we read its outputs (mask lists, operands), so wait for it to complete.
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -434,7 +438,17 @@ void launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
     if (grid <= 0) return;
     GemmArgs a = args;
     a.sched = sched_slot();
-    kern<<<grid, kThreads, kSmemBytes, s>>>(ta, tb, tout, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, tout, a), "sd_gemm_kernel launch");
     check_cuda(cudaGetLastError(), "sd_gemm_kernel launch");
     note_launch();
 }

@@ -125,6 +125,11 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     int blk = blockIdx.x;
+    // the consumer GEMM may start its prologue now; its griddepcontrol.wait
+    // still orders all of its reads after this grid completes
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // our own inputs (mask words in compact mode) come from earlier work
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (blk < a.nb_words) {
         // ---- words: one warp per 64-bit word, two bits per lane, ballot-packed
@@ -279,8 +284,17 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
             raised = true;
         }
     }
-    mask_plan_kernel<<<grid, kThreads, smem, s>>>(a);
-    check_cuda(cudaGetLastError(), "mask_plan_kernel launch");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, mask_plan_kernel, a), "mask_plan_kernel launch");
     note_launch();
 }
 
