@@ -272,9 +272,17 @@ def main():
     def flush():
         flush_buf.fill_(float(len(str(flush_buf.numel()))))
 
-    def time_steps(step, steps, warmup):
+    def time_steps(step, steps, warmup, preroll_s=0.3):
         """Sum of per-step CUDA-event durations on the launching stream (L2 flushed
-        before every step, outside the events); max over ranks."""
+        before every step, outside the events); max over ranks. A short sustained
+        pre-roll of the same step first, so every configuration is timed in the
+        same (power-capped) steady state rather than a cold burst."""
+        t_end, j = time.time() + preroll_s, 0
+        while time.time() < t_end:
+            step(j)
+            j += 1
+            if j % 64 == 0:
+                torch.cuda.synchronize()
         for i in range(warmup):
             flush()
             step(i)
@@ -349,13 +357,7 @@ def main():
     with ClockSampler(local_rank) as clk:
         # sustained load first (~1.5 s of the same step) so the 100 ms nvidia-smi
         # samples see the clocks the timed steps run at
-        t_end, i = time.time() + (0.2 if args.profile else 1.5), 0
-        while time.time() < t_end:
-            head_step(i)
-            i += 1
-            if i % 64 == 0:
-                torch.cuda.synchronize()
-        ms = time_steps(head_step, args.steps, args.warmup)
+        ms = time_steps(head_step, args.steps, args.warmup, preroll_s=0.2 if args.profile else 1.5)
     gpu_launches = launch_box[0]  # our kernels enqueued inside the timed region (4 per step)
     plan = plan_for(args.p)
     keep = plan.mask.keep_count() / plan.mask.total_blocks()

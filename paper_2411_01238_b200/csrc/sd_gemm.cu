@@ -24,8 +24,10 @@
 //   warps 4..7  epilogue: tcgen05.ld -> scale -> bf16/fp32 -> swizzled smem
 //               -> TMA store; all-dropped tiles written as +0.0 directly.
 // Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
-// Every role walks the same static unit sequence (u = blockIdx.x + i*gridDim.x),
-// so no scheduling state crosses roles; zero-work units skip TMEM entirely.
+// Scheduling is dynamic: the producer steals units from a global atomic counter
+// (units ordered heaviest first, grouped for L2 reuse), decodes them (list
+// lookups) and hands the decoded unit to the MMA and epilogue roles through a
+// shared-memory ring; zero-work units skip TMEM entirely.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -48,16 +50,19 @@ constexpr int kOffA = 0;
 constexpr int kOffB = kOffA + kStages * kABytes;
 constexpr int kOffEpi = kOffB + kStages * kBBytes;
 constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+constexpr int kGroupRows = 16;  // tile rows per rasterization group
 constexpr int kSchedDepth = 4;  // unit-index ring between the producer and the consumers
 constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth;
 constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
 constexpr int kOffSched = kOffTmemSlot + 16;
-constexpr int kSmemBytes = kOffSched + 4 * kSchedDepth + 1024;  // + alignment slack
+constexpr int kUnitInts = 12;  // sizeof(Unit) / 4
+constexpr int kSmemBytes = kOffSched + 4 * kUnitInts * kSchedDepth + 1024;  // + alignment slack
 
 static_assert(kSmemBytes <= 232448, "shared memory budget");
+static_assert(kUnitInts * 4 == 48, "Unit layout");
 
 struct Unit {
-    int row0;      // first output row
+    int row0;      // first output row; -1 = end of work
     int list_row;  // mask row (list index) of this tile row
     int n0;        // first output column (dsd)
     int n_eff;     // MMA N; 0 => no MMA work
@@ -71,18 +76,17 @@ struct Unit {
 template <bool SDD>
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
     Unit t;
-    // dsd: row-major over (tile row, column unit), tile rows heaviest first.
-    // sdd: column-unit-major, so the units that carry MMA work (low unit index
-    //      within a row: kept blocks are packed first) are handed out first and
-    //      the zero-fill-only units last.
-    int i, cu;
-    if constexpr (!SDD) {
-        i = u / a.n_col_units;
-        cu = u - i * a.n_col_units;
-    } else {
-        cu = u / a.n_row_tiles;
-        i = u - cu * a.n_row_tiles;
-    }
+    // Grouped rasterization: tile rows (sorted heaviest first) are taken in
+    // groups of kGroupRows; inside a group units go column-unit-major. The
+    // CTAs in flight then share a few operand column/row slabs (L2 reuse), heavy
+    // groups still go first, and for sdd the units carrying MMA work (kept
+    // blocks are packed into the low column units) precede the zero-fill-only
+    // units of their group.
+    const int g = u / (kGroupRows * a.n_col_units);
+    const int rem_u = u - g * kGroupRows * a.n_col_units;
+    const int rows_in_group = min(kGroupRows, a.n_row_tiles - g * kGroupRows);
+    const int cu = rem_u / rows_in_group;
+    const int i = g * kGroupRows + (rem_u - cu * rows_in_group);
     const int rt = a.row_order ? __ldg(a.row_order + i) : i;
     t.row0 = rt * kBM;
     t.list_row = t.row0 / a.out_row_blk;
@@ -149,7 +153,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* sfull_bar = bars + 2 * kStages + 4;
     uint64_t* sempty_bar = sfull_bar + kSchedDepth;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
-    volatile int* sched_unit = reinterpret_cast<volatile int*>(smem + kOffSched);
+    // ring of decoded units: the producer decodes (global loads), the MMA and
+    // epilogue roles read the decoded unit from shared memory
+    Unit* sched_unit = reinterpret_cast<Unit*>(smem + kOffSched);
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
@@ -195,30 +201,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             // stealing through a global atomic counter (units are ordered
             // heaviest first, so this is greedy longest-processing-time).
             int u = blockIdx.x;
+            int nxt = u < num_units ? static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u))
+                                    : num_units;
+            Unit t;
+            if (u < num_units) t = decode_unit<SDD>(args, u); else t.row0 = -1;
             while (true) {
                 ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1);
-                sched_unit[sslot] = u;
+                sched_unit[sslot] = t;
                 ptx::mbar_arrive(sfull_bar + sslot);
                 if (++sslot == kSchedDepth) {
                     sslot = 0;
                     sphase ^= 1;
                 }
-                if (u >= num_units) break;
-                const int next = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u));
-                const Unit t = decode_unit<SDD>(args, u);
-                u = next;
-                if (t.n_eff == 0) continue;
-                const uint32_t tx_bytes = kABytes + t.n_eff * kBK * 2;
+                if (t.row0 < 0) break;
+                // decode the next unit now: its global loads (and the atomic
+                // for the one after) overlap this unit's TMA stream
+                const Unit cur = t;
+                u = nxt;
+                if (u < num_units) {
+                    nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u));
+                    t = decode_unit<SDD>(args, u);
+                } else {
+                    t.row0 = -1;
+                }
+                if (cur.n_eff == 0) continue;
+                const uint32_t tx_bytes = kABytes + cur.n_eff * kBK * 2;
                 const int spb = args.red_blk / kBK;
-                for (int s = 0; s < t.nstages; ++s) {
+                const int32_t* lst =
+                    args.list_idx ? args.list_idx + static_cast<int64_t>(cur.list_row) * args.list_stride : nullptr;
+                // kept-block index prefetched one block ahead (off the TMA issue path)
+                int kb_next = (!SDD && lst) ? __ldg(lst) : 0;
+                int kb = 0;
+                for (int s = 0, li = 0, sub = 0; s < cur.nstages; ++s) {
                     int r0;
                     if constexpr (!SDD) {
-                        const int li = s / spb;
-                        const int kb = args.list_idx
-                                           ? __ldg(args.list_idx +
-                                                   static_cast<int64_t>(t.list_row) * args.list_stride + li)
-                                           : li;
-                        r0 = kb * args.red_blk + (s - li * spb) * kBK;
+                        if (sub == 0) {
+                            kb = lst ? kb_next : li;
+                            if (lst && li + 1 < cur.nstages / spb) kb_next = __ldg(lst + li + 1);
+                        }
+                        r0 = kb * args.red_blk + sub * kBK;
+                        if (++sub == spb) {
+                            sub = 0;
+                            ++li;
+                        }
                     } else {
                         r0 = s * kBK;
                     }
@@ -228,22 +253,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sA = smem + kOffA + stage * kABytes;
                     uint8_t* sB = smem + kOffB + stage * kBBytes;
                     if constexpr (!A_MN) {
-                        ptx::tma_load_2d(&tmA, fb, sA, r0, t.row0, pol);
+                        ptx::tma_load_2d(&tmA, fb, sA, r0, cur.row0, pol);
                     } else {
-                        ptx::tma_load_2d(&tmA, fb, sA, t.row0, r0, pol);
-                        ptx::tma_load_2d(&tmA, fb, sA + 8192, t.row0 + 64, r0, pol);
+                        ptx::tma_load_2d(&tmA, fb, sA, cur.row0, r0, pol);
+                        ptx::tma_load_2d(&tmA, fb, sA + 8192, cur.row0 + 64, r0, pol);
                     }
                     if constexpr (!SDD) {
                         if constexpr (!B_MN) {
-                            for (int j = 0; j < t.n_eff / 128; ++j)
-                                ptx::tma_load_2d(&tmB, fb, sB + j * 16384, r0, t.n0 + 128 * j, pol);
+                            for (int j = 0; j < cur.n_eff / 128; ++j)
+                                ptx::tma_load_2d(&tmB, fb, sB + j * 16384, r0, cur.n0 + 128 * j, pol);
                         } else {
-                            for (int j = 0; j < t.n_eff / 64; ++j)
-                                ptx::tma_load_2d(&tmB, fb, sB + j * 8192, t.n0 + 64 * j, r0, pol);
+                            for (int j = 0; j < cur.n_eff / 64; ++j)
+                                ptx::tma_load_2d(&tmB, fb, sB + j * 8192, cur.n0 + 64 * j, r0, pol);
                         }
                     } else {
-                        for (int sl = 0; sl < t.nslots; ++sl) {
-                            const int col0 = t.slot_blk[sl] * args.out_col_blk;
+                        for (int sl = 0; sl < cur.nslots; ++sl) {
+                            const int col0 = cur.slot_blk[sl] * args.out_col_blk;
                             if constexpr (!B_MN) {
                                 const int per = args.out_col_blk / 128;
                                 for (int j = 0; j < per; ++j)
@@ -274,14 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t sphase = 0;
             while (true) {
                 ptx::mbar_wait(sfull_bar + sslot, sphase);
-                const int u = sched_unit[sslot];
+                const Unit t = sched_unit[sslot];
                 ptx::mbar_arrive(sempty_bar + sslot);
                 if (++sslot == kSchedDepth) {
                     sslot = 0;
                     sphase ^= 1;
                 }
-                if (u >= num_units) break;
-                const Unit t = decode_unit<SDD>(args, u);
+                if (t.row0 < 0) break;
                 if (t.n_eff == 0) continue;
                 const uint32_t acc = acc_iter & 1;
                 const uint32_t acc_phase = (acc_iter >> 1) & 1;
@@ -327,15 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sphase = 0;
         while (true) {
             ptx::mbar_wait(sfull_bar + sslot, sphase);
-            const int u = sched_unit[sslot];
+            const Unit t = sched_unit[sslot];
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(sempty_bar + sslot);
             if (++sslot == kSchedDepth) {
                 sslot = 0;
                 sphase ^= 1;
             }
-            if (u >= num_units) break;
-            const Unit t = decode_unit<SDD>(args, u);
+            if (t.row0 < 0) break;
             const int row_first = t.row0 + 32 * q;
             if constexpr (SDD) {
                 for (int z = 0; z < t.nzero; ++z)
