@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (headline loop only)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (CI check of the data-parallel path)")
     return ap.parse_args()
 
 
@@ -232,10 +234,15 @@ def main():
 
     import paper_2411_01238_b200 as sd
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ndev = max(torch.cuda.device_count(), 1)
+    dev_index = local_rank % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -354,7 +361,7 @@ def main():
 
     # ---- headline: sparse fwd+bwd at args.p
     head_step = sparse_step_fn(args.p)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         # sustained load first (~1.5 s of the same step) so the 100 ms nvidia-smi
         # samples see the clocks the timed steps run at
         ms = time_steps(head_step, args.steps, args.warmup, preroll_s=0.2 if args.profile else 1.5)

@@ -74,6 +74,15 @@ SD_API const char* sd_last_error(void);
 /* Number of usable sm_100 devices (0 when none: compute calls then fail). */
 SD_API int sd_device_count(void);
 
+/* Minimal device-memory plumbing so FFI callers (and the C++ wrapper
+ * include/sparsedrop_b200.hpp) need no CUDA headers. kind: 0 host->device,
+ * 1 device->host, 2 device->device. stream may be NULL (legacy stream). */
+SD_API int sd_device_alloc(void** ptr, size_t bytes);
+SD_API int sd_device_free(void* ptr);
+SD_API int sd_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);
+SD_API int sd_memset(void* dst, int32_t value, size_t bytes, void* stream);
+SD_API int sd_stream_synchronize(void* stream);
+
 /* Workspace size for a block_rows x block_cols mask and its compaction lists. */
 SD_API size_t sd_mask_workspace_bytes(int32_t block_rows, int32_t block_cols);
 /* Carve `workspace` into the mask's arrays and record the geometry

@@ -50,6 +50,11 @@ PROTOTYPES = {
     "sd_last_error": (ctypes.c_char_p, []),
     "sd_device_count": (ctypes.c_int, []),
     "sd_launch_count": (ctypes.c_uint64, []),
+    "sd_device_alloc": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_size_t]),
+    "sd_device_free": (ctypes.c_int, [_P]),
+    "sd_memcpy": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _I, _P]),
+    "sd_memset": (ctypes.c_int, [_P, _I, ctypes.c_size_t, _P]),
+    "sd_stream_synchronize": (ctypes.c_int, [_P]),
     "sd_mask_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
     "sd_mask_bind": (ctypes.c_int, [_MASKP, _P, _I, _I, _I, _I, _I]),
     "sd_mask_sample": (ctypes.c_int, [_MASKP, ctypes.c_uint64, ctypes.c_double, _I, _I, _P]),

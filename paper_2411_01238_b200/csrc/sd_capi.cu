@@ -249,6 +249,40 @@ int sd_device_count(void) {
     return ok;
 }
 
+int sd_device_alloc(void** ptr, size_t bytes) {
+    return guarded([&] {
+        if (!ptr) fail(SD_EINVAL, "sd_device_alloc: null out pointer");
+        require_device();
+        check_cuda(cudaMalloc(ptr, bytes), "cudaMalloc");
+    });
+}
+
+int sd_device_free(void* ptr) {
+    return guarded([&] {
+        if (ptr) check_cuda(cudaFree(ptr), "cudaFree");
+    });
+}
+
+int sd_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream) {
+    return guarded([&] {
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                 : kind == 1 ? cudaMemcpyDeviceToHost
+                                 : kind == 2 ? cudaMemcpyDeviceToDevice
+                                             : cudaMemcpyDefault;
+        if (kind < 0 || kind > 2) fail(SD_EINVAL, "sd_memcpy: kind must be 0, 1 or 2");
+        check_cuda(cudaMemcpyAsync(dst, src, bytes, k, as_stream(stream)), "cudaMemcpyAsync");
+        if (kind == 1 && !stream) check_cuda(cudaStreamSynchronize(nullptr), "cudaStreamSynchronize");
+    });
+}
+
+int sd_memset(void* dst, int32_t value, size_t bytes, void* stream) {
+    return guarded([&] { check_cuda(cudaMemsetAsync(dst, value, bytes, as_stream(stream)), "cudaMemsetAsync"); });
+}
+
+int sd_stream_synchronize(void* stream) {
+    return guarded([&] { check_cuda(cudaStreamSynchronize(as_stream(stream)), "cudaStreamSynchronize"); });
+}
+
 // Layout of the mask workspace (each array 256-byte aligned):
 // words | keep_count | ticket | row_cnt | row_idx | col_cnt | col_idx | row_order | col_order
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
