@@ -26,8 +26,8 @@ def test_bench_two_ranks():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--size", "1024", "--no-sweep", "--no-e2e", "--no-cpu",
-           "--dist-backend", "gloo"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+           "--dist-backend", "gloo", "--preroll", "0"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
                        env={**os.environ, "OMP_NUM_THREADS": "2"})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
