@@ -395,14 +395,10 @@ int sd_mask_retile(const sd_block_mask* in, int32_t split_m, int32_t split_k, sd
 namespace sd {
 namespace {
 
-// A fully validated, ready-to-launch GEMM (tensor maps encoded).
-struct GemmCall {
-    bool a_mn = false, b_mn = false, f32 = false;
-    GemmKind kind = GemmKind::dsd;
-    CUtensorMap ta, tb, tout;
-    GemmArgs args;
-    void launch(cudaStream_t s) const { launch_gemm(a_mn, b_mn, kind, f32, ta, tb, tout, args, s); }
-};
+uint32_t flags_of(bool a_mn, bool b_mn, bool sdd, int out_dtype) {
+    return (a_mn ? kFlagAMN : 0u) | (b_mn ? kFlagBMN : 0u) | (sdd ? kFlagSDD : 0u) |
+           (out_dtype == SD_DTYPE_F32 ? kFlagF32 : 0u);
+}
 
 // dense c[m,n] = A * B with A (K-major | MN-major) and B (K-major | MN-major)
 GemmCall prep_dense(const void* a, bool a_mn, const void* b, bool b_mn, void* c, int c_dtype, int m, int n,
@@ -410,14 +406,11 @@ GemmCall prep_dense(const void* a, bool a_mn, const void* b, bool b_mn, void* c,
     check_gemm(m, n, k);
     check_ptr(a, "a"), check_ptr(b, "b"), check_ptr(c, "c"), check_dtype(c_dtype);
     GemmCall g;
-    g.a_mn = a_mn;
-    g.b_mn = b_mn;
-    g.f32 = c_dtype == SD_DTYPE_F32;
-    g.kind = GemmKind::dsd;
     g.ta = a_mn ? mnmajor_map(a, m, k) : kmajor_map(a, k, m);
     g.tb = b_mn ? mnmajor_map(b, n, k) : kmajor_map(b, k, n);
     g.tout = out_map(c, c_dtype, m, n);
     g.args = base_args(m, n, k, 1.0f, c);
+    g.args.flags = flags_of(a_mn, b_mn, false, c_dtype);
     return g;
 }
 
@@ -433,14 +426,11 @@ GemmCall prep_dsd_forward(const void* a, const sd_block_mask* mask, const void* 
     check_row_blk(mask->m_blk, "m_blk");
     check_red_blk(mask->k_blk, "k_blk");
     GemmCall g;
-    g.a_mn = false;
-    g.b_mn = true;
-    g.f32 = c_dtype == SD_DTYPE_F32;
-    g.kind = GemmKind::dsd;
     g.ta = kmajor_map(a, k, m);
     g.tb = mnmajor_map(b, n, k);
     g.tout = out_map(c, c_dtype, m, n);
     g.args = base_args(m, n, k, scale, c);
+    g.args.flags = flags_of(false, true, false, c_dtype);
     g.args.list_cnt = mask->row_cnt;
     g.args.list_idx = mask->row_idx;
     g.args.list_stride = mask->block_cols;
@@ -464,14 +454,11 @@ GemmCall prep_sdd(const void* a, const void* b, bool b_kmajor, const sd_block_ma
     check_row_blk(mask->m_blk, "m_blk");
     check_col_blk(mask->k_blk, "n_blk");
     GemmCall g;
-    g.a_mn = false;
-    g.b_mn = !b_kmajor;
-    g.f32 = c_dtype == SD_DTYPE_F32;
-    g.kind = GemmKind::sdd;
     g.ta = kmajor_map(a, k, m);
     g.tb = b_kmajor ? kmajor_map(b, k, n) : mnmajor_map(b, n, k);
     g.tout = out_map(c, c_dtype, m, n);
     g.args = base_args(m, n, k, scale, c);
+    g.args.flags = flags_of(false, !b_kmajor, true, c_dtype);
     g.args.words = mask->words;
     g.args.list_cnt = mask->row_cnt;
     g.args.list_idx = mask->row_idx;
@@ -503,14 +490,11 @@ GemmCall prep_layer_dw(const void* x, const sd_block_mask* mask, const void* dy,
     check_row_blk(mask->k_blk, "k_blk");
     check_red_blk(mask->m_blk, "m_blk");
     GemmCall g;
-    g.a_mn = true;
-    g.b_mn = true;
-    g.f32 = dw_dtype == SD_DTYPE_F32;
-    g.kind = GemmKind::dsd;
     g.ta = mnmajor_map(x, k, m);
     g.tb = mnmajor_map(dy, n, m);
     g.tout = out_map(dw, dw_dtype, k, n);
     g.args = base_args(k, n, m, scale, dw);
+    g.args.flags = flags_of(true, true, false, dw_dtype);
     g.args.list_cnt = mask->col_cnt;
     g.args.list_idx = mask->col_idx;
     g.args.list_stride = mask->block_rows;
@@ -540,22 +524,19 @@ struct sd_layer_plan {
     uint64_t threshold;
     int device;
     sd::GemmCall fwd, dw, dx, dense_fwd, dense_dw, dense_dx;
-    // backward fork/join: dX runs on `aux` concurrently with dW on the caller's
-    // stream, so each persistent kernel's CTAs fill the other's tail
+    // (kept for ABI compatibility of the plan object; unused since the backward
+    // runs as one fused launch)
     cudaStream_t aux = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
-// Enqueue `first` on s and `second` on the plan's auxiliary stream, both after
-// everything already on s; s waits for both.
-void fork_join(sd_layer_plan* plan, const sd::GemmCall& first, const sd::GemmCall& second, cudaStream_t s) {
-    sd::check_cuda(cudaEventRecord(plan->fork, s), "cudaEventRecord(fork)");
-    sd::check_cuda(cudaStreamWaitEvent(plan->aux, plan->fork, 0), "cudaStreamWaitEvent(aux)");
-    second.launch(plan->aux);
-    first.launch(s);
-    sd::check_cuda(cudaEventRecord(plan->join, plan->aux), "cudaEventRecord(join)");
-    sd::check_cuda(cudaStreamWaitEvent(s, plan->join, 0), "cudaStreamWaitEvent(join)");
+// The backward's two GEMMs are independent: run them as ONE persistent launch
+// with a shared heaviest-first queue — dX's coarse full-reduction units first,
+// dW's finer units fill the tail.
+void fused_backward(const sd::GemmCall& dx, const sd::GemmCall& dw, cudaStream_t s) {
+    const sd::GemmCall* calls[2] = {&dx, &dw};
+    sd::launch_gemms(calls, 2, s);
 }
 }  // namespace
 
@@ -566,7 +547,7 @@ int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_
     return guarded([&] {
         auto g = prep_dense(a, false, b, true, c, c_dtype, m, n, k);
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -575,7 +556,7 @@ int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, i
     return guarded([&] {
         auto g = prep_dense(a, false, b_t, false, c, c_dtype, m, n, k);
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -584,7 +565,7 @@ int sd_dense_gemm_tn(const void* a_t, const void* b, void* c, int32_t c_dtype, i
     return guarded([&] {
         auto g = prep_dense(a_t, true, b, true, c, c_dtype, m, n, k);
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -594,7 +575,7 @@ int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float
     return guarded([&] {
         auto g = prep_dsd_forward(a, mask, b, scale, c, c_dtype, m, n, k, counters, "dsd_matmul");
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -603,7 +584,7 @@ int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, f
     return guarded([&] {
         auto g = prep_dsd_forward(x, mask, w, scale, y, y_dtype, m, n, k, nullptr, "layer forward");
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -613,7 +594,7 @@ int sd_sdd_matmul(const void* a, const void* b, const sd_block_mask* mask, float
     return guarded([&] {
         auto g = prep_sdd(a, b, false, mask, scale, c, c_dtype, m, n, k, counters, "sdd_matmul");
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -622,7 +603,7 @@ int sd_linear_backward_dx(const void* dy, const void* w, const sd_block_mask* ma
     return guarded([&] {
         auto g = prep_layer_dx(dy, w, mask, scale, dx, dx_dtype, m, n, k);
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -631,7 +612,7 @@ int sd_linear_backward_dw(const void* x, const sd_block_mask* mask, const void* 
     return guarded([&] {
         auto g = prep_layer_dw(x, mask, dy, scale, dw, dw_dtype, m, n, k);
         require_device();
-        g.launch(as_stream(stream));
+        launch_gemm(g, as_stream(stream));
     });
 }
 
@@ -663,9 +644,6 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
-        check_cuda(cudaStreamCreateWithFlags(&tmp.aux, cudaStreamNonBlocking), "cudaStreamCreate(aux)");
-        check_cuda(cudaEventCreateWithFlags(&tmp.fork, cudaEventDisableTiming), "cudaEventCreate");
-        check_cuda(cudaEventCreateWithFlags(&tmp.join, cudaEventDisableTiming), "cudaEventCreate");
         *out = new sd_layer_plan(tmp);
     });
 }
@@ -674,44 +652,42 @@ int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, as_stream(stream));
-        plan->fwd.launch(as_stream(stream));
+        launch_gemm(plan->fwd, as_stream(stream));
     });
 }
 
 int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        plan->dw.launch(as_stream(stream));
+        launch_gemm(plan->dw, as_stream(stream));
     });
 }
 
 int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        plan->dx.launch(as_stream(stream));
+        launch_gemm(plan->dx, as_stream(stream));
     });
 }
 
 int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        // dX (coarse units: full-N reductions) starts first on the aux stream;
-        // dW's finer units fill its tail.
-        fork_join(plan, plan->dw, plan->dx, as_stream(stream));
+        fused_backward(plan->dx, plan->dw, as_stream(stream));
     });
 }
 
 int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        plan->dense_fwd.launch(as_stream(stream));
+        launch_gemm(plan->dense_fwd, as_stream(stream));
     });
 }
 
 int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        fork_join(plan, plan->dense_dw, plan->dense_dx, as_stream(stream));
+        fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream));
     });
 }
 

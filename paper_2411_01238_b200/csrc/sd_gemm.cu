@@ -1,7 +1,9 @@
 // sd_gemm.cu — the SparseDrop tensor-core GEMMs for sm_100a.
 //
-// One persistent, warp-specialised tcgen05 kernel, templated on operand
-// major-ness and on how the block mask enters, serves every GEMM of the path:
+// One persistent, warp-specialised tcgen05 kernel serves every GEMM of the
+// path; operand major-ness and the way the block mask enters are per-problem
+// run-time flags, and one launch may carry TWO independent problems sharing one
+// work queue (the backward's dW and dX):
 //
 //   dsd (reduction-block skipping, gemm.hpp:133-170):
 //     forward  Y  = s (X (.) m) W      A = X  K-major, B = W  MN-major, row lists
@@ -13,7 +15,7 @@
 //
 // Tile: 128 output rows (one tcgen05 M=128 MMA, TMEM lanes = rows) x up to 256
 // output columns (MMA N chosen per tile at run time: 256, or 128 for a ragged
-// edge / a half-kept sdd pair). Reduction in 64-element stages = one 128-byte
+// edge / an odd kept sdd block). Reduction in 64-element stages = one 128-byte
 // swizzle atom; a 128-wide mask block is two stages (the paper's retile(1,2),
 // PAPER.md:149-151). Only kept reduction blocks are ever loaded by TMA.
 //
@@ -25,15 +27,34 @@
 //               -> TMA store; all-dropped tiles written as +0.0 directly.
 // Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
 // Scheduling is dynamic: the producer steals units from a global atomic counter
-// (units ordered heaviest first, grouped for L2 reuse), decodes them (list
-// lookups) and hands the decoded unit to the MMA and epilogue roles through a
-// shared-memory ring; zero-work units skip TMEM entirely.
+// (units ordered heaviest first, grouped for L2 reuse; problem 0 before problem
+// 1), decodes them (list lookups) and hands the decoded unit to the MMA and
+// epilogue roles through a shared-memory ring; zero-work units skip TMEM.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "sd_internal.h"
 #include "sd_ptx.cuh"
+
+// Optional instrumentation (build with -DSD_TRACE, `make trace`): per-CTA
+// cycle counters of every wait, read back with sd_trace_read().
+#ifdef SD_TRACE
+constexpr int kTraceSlots = 16;
+__device__ unsigned long long g_sd_trace[1024 * kTraceSlots];
+#define SD_TWAIT(slot, expr)                          \
+    do {                                              \
+        const long long t0_ = clock64();              \
+        expr;                                         \
+        tr[slot] += clock64() - t0_;                  \
+    } while (0)
+#define SD_TADD(slot, v) tr[slot] += (v)
+#else
+#define SD_TWAIT(slot, expr) expr
+#define SD_TADD(slot, v) ((void)0)
+#endif
 
 namespace sd {
 namespace {
@@ -45,24 +66,21 @@ constexpr int kEpiWarps = 4;
 constexpr int kEpiBufBytes = 32 * 128;  // one warp's 32 rows x 128 B store box
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
+constexpr int kMaxProblems = 2;
 
 constexpr int kOffA = 0;
 constexpr int kOffB = kOffA + kStages * kABytes;
 constexpr int kOffEpi = kOffB + kStages * kBBytes;
 constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
 constexpr int kGroupRows = 16;  // tile rows per rasterization group
-constexpr int kSchedDepth = 4;  // unit-index ring between the producer and the consumers
+constexpr int kSchedDepth = 4;  // decoded-unit ring between the producer and the consumers
 constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth;
 constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
 constexpr int kOffSched = kOffTmemSlot + 16;
-constexpr int kUnitInts = 12;  // sizeof(Unit) / 4
-constexpr int kSmemBytes = kOffSched + 4 * kUnitInts * kSchedDepth + 1024;  // + alignment slack
-
-static_assert(kSmemBytes <= 232448, "shared memory budget");
-static_assert(kUnitInts * 4 == 48, "Unit layout");
 
 struct Unit {
-    int row0;      // first output row; -1 = end of work
+    int prob;      // problem index; -1 = end of work
+    int row0;      // first output row
     int list_row;  // mask row (list index) of this tile row
     int n0;        // first output column (dsd)
     int n_eff;     // MMA N; 0 => no MMA work
@@ -71,11 +89,27 @@ struct Unit {
     int slot_blk[2];
     int nzero;     // sdd: dropped output blocks in this unit
     int zero_blk[2];
+    int pad[4];
+};
+static_assert(sizeof(Unit) == 64, "Unit layout");
+
+constexpr int kSmemBytes = kOffSched + static_cast<int>(sizeof(Unit)) * kSchedDepth + 1024;  // + align slack
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+struct LaunchArgs {
+    GemmArgs p[kMaxProblems];
+    int nprob;
+    int total_units;
+    unsigned int* sched;  // {next-unit counter, CTAs-done counter}
 };
 
-template <bool SDD>
-__device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
+struct TensorMaps {
+    CUtensorMap m[3 * kMaxProblems];  // A, B, Out per problem
+};
+
+__device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) {
     Unit t;
+    t.prob = prob;
     // Grouped rasterization: tile rows (sorted heaviest first) are taken in
     // groups of kGroupRows; inside a group units go column-unit-major. The
     // CTAs in flight then share a few operand column/row slabs (L2 reuse), heavy
@@ -92,7 +126,7 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
     t.list_row = t.row0 / a.out_row_blk;
     t.nslots = 0;
     t.nzero = 0;
-    if constexpr (!SDD) {
+    if (!(a.flags & kFlagSDD)) {
         t.n0 = cu * kBN;
         const int rem = a.cols_out - t.n0;
         t.n_eff = rem < kBN ? rem : kBN;
@@ -120,6 +154,11 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int u) {
     return t;
 }
 
+__device__ __forceinline__ Unit decode_global(const LaunchArgs& L, int u) {
+    if (L.nprob > 1 && u >= L.p[1].unit_begin) return decode_unit(L.p[1], 1, u - L.p[1].unit_begin);
+    return decode_unit(L.p[0], 0, u);
+}
+
 // Zero a 32-row x `ncols` slab of the output with coalesced 16-byte stores.
 template <bool OUT_F32>
 __device__ __forceinline__ void zero_rows(const GemmArgs& a, int row_first, int col0, int ncols,
@@ -136,10 +175,86 @@ __device__ __forceinline__ void zero_rows(const GemmArgs& a, int row_first, int 
     }
 }
 
-template <bool A_MN, bool B_MN, bool SDD, bool OUT_F32>
+// Epilogue of one unit for one warp (32 output rows).
+template <bool OUT_F32>
+__device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorMap* tmOut, const Unit& t,
+                                              uint32_t q, uint32_t lane, uint32_t tmem_base,
+                                              uint64_t* tfull_bar, uint64_t* tempty_bar, uint8_t* ebuf,
+                                              uint32_t ebuf_addr, uint32_t& bi, uint32_t& acc_iter,
+                                              long long* tr) {
+    (void)tr;
+    constexpr int kChunkCols = OUT_F32 ? 32 : 64;  // 128 bytes of output per row
+    const bool sdd = a.flags & kFlagSDD;
+    const int row_first = t.row0 + 32 * q;
+    if (sdd) {
+        for (int z = 0; z < t.nzero; ++z)
+            zero_rows<OUT_F32>(a, row_first, t.zero_blk[z] * a.out_col_blk, a.out_col_blk, lane);
+    }
+    if (t.n_eff == 0) {
+        if (!sdd) {
+            const int rem = a.cols_out - t.n0;
+            zero_rows<OUT_F32>(a, row_first, t.n0, rem < kBN ? rem : kBN, lane);
+        }
+        return;
+    }
+    const uint32_t acc = acc_iter & 1;
+    const uint32_t acc_phase = (acc_iter >> 1) & 1;
+    ++acc_iter;
+    SD_TWAIT(5, ptx::mbar_wait(tfull_bar + acc, acc_phase));
+    ptx::tc_fence_after();
+    const int nchunks = t.n_eff / kChunkCols;
+    for (int c = 0; c < nchunks; ++c) {
+        const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kBN + c * kChunkCols;
+        uint32_t v[kChunkCols];
+        ptx::tmem_ld_32x32b_x32(taddr, v);
+        if constexpr (!OUT_F32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
+        ptx::tmem_ld_wait();
+        if (c == nchunks - 1) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty_bar + acc);
+        }
+        // staging buffer bi must no longer be read by the TMA store issued 2 chunks ago
+        if (lane == 0) ptx::bulk_wait_group_read<1>();
+        __syncwarp();
+        const uint32_t row_addr = ebuf_addr + bi * kEpiBufBytes + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint32_t w0, w1, w2, w3;
+            if constexpr (OUT_F32) {
+                w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * a.scale);
+                w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * a.scale);
+                w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * a.scale);
+                w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * a.scale);
+            } else {
+                const float* f = reinterpret_cast<const float*>(v) + 8 * j;
+                w0 = ptx::pack_bf16x2(f[0] * a.scale, f[1] * a.scale);
+                w1 = ptx::pack_bf16x2(f[2] * a.scale, f[3] * a.scale);
+                w2 = ptx::pack_bf16x2(f[4] * a.scale, f[5] * a.scale);
+                w3 = ptx::pack_bf16x2(f[6] * a.scale, f[7] * a.scale);
+            }
+            ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), w0, w1, w2, w3);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            int col;
+            if (sdd) {
+                const int tcol = c * kChunkCols;
+                const int sl = tcol / a.out_col_blk;
+                col = t.slot_blk[sl] * a.out_col_blk + (tcol - sl * a.out_col_blk);
+            } else {
+                col = t.n0 + c * kChunkCols;
+            }
+            ptx::tma_store_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
+            ptx::bulk_commit_group();
+        }
+        bi ^= 1;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-    sd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmOut, const GemmArgs args) {
+    sd_gemm_kernel(const __grid_constant__ TensorMaps tms, const __grid_constant__ LaunchArgs L) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -153,18 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* sfull_bar = bars + 2 * kStages + 4;
     uint64_t* sempty_bar = sfull_bar + kSchedDepth;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
-    // ring of decoded units: the producer decodes (global loads), the MMA and
-    // epilogue roles read the decoded unit from shared memory
     Unit* sched_unit = reinterpret_cast<Unit*>(smem + kOffSched);
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
-    const int num_units = args.n_row_tiles * args.n_col_units;
+    const int num_units = L.total_units;
 
     if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmA);
-        ptx::prefetch_tmap(&tmB);
-        ptx::prefetch_tmap(&tmOut);
+        for (int i = 0; i < 3 * L.nprob; ++i) ptx::prefetch_tmap(&tms.m[i]);
         for (int i = 0; i < kStages; ++i) {
             ptx::mbar_init(full_bar + i, 1);
             ptx::mbar_init(empty_bar + i, 1);
@@ -188,9 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // we read its outputs (mask lists, operands), so wait for it to complete.
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
+    long long tr[16] = {0};
+#ifdef SD_TRACE
+    const long long t_start = clock64();
+#endif
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (+ scheduler) =====================
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_normal();
             int stage = 0;
@@ -201,45 +316,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             // stealing through a global atomic counter (units are ordered
             // heaviest first, so this is greedy longest-processing-time).
             int u = blockIdx.x;
-            int nxt = u < num_units ? static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u))
-                                    : num_units;
+            int nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
             Unit t;
-            if (u < num_units) t = decode_unit<SDD>(args, u); else t.row0 = -1;
+            if (u < num_units) t = decode_global(L, u); else t.prob = -1;
             while (true) {
-                ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1);
+                SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
                 sched_unit[sslot] = t;
                 ptx::mbar_arrive(sfull_bar + sslot);
                 if (++sslot == kSchedDepth) {
                     sslot = 0;
                     sphase ^= 1;
                 }
-                if (t.row0 < 0) break;
+                if (t.prob < 0) break;
                 // decode the next unit now: its global loads (and the atomic
                 // for the one after) overlap this unit's TMA stream
                 const Unit cur = t;
                 u = nxt;
                 if (u < num_units) {
-                    nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(args.sched, 1u));
-                    t = decode_unit<SDD>(args, u);
+                    nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
+                    t = decode_global(L, u);
                 } else {
-                    t.row0 = -1;
+                    t.prob = -1;
                 }
                 if (cur.n_eff == 0) continue;
+                const GemmArgs& a = L.p[cur.prob];
+                const CUtensorMap* tmA = &tms.m[3 * cur.prob];
+                const CUtensorMap* tmB = &tms.m[3 * cur.prob + 1];
+                const bool a_mn = a.flags & kFlagAMN;
+                const bool b_mn = a.flags & kFlagBMN;
+                const bool sdd = a.flags & kFlagSDD;
                 const uint32_t tx_bytes = kABytes + cur.n_eff * kBK * 2;
-                const int spb = args.red_blk / kBK;
+                const int spb = a.red_blk / kBK;
                 const int32_t* lst =
-                    args.list_idx ? args.list_idx + static_cast<int64_t>(cur.list_row) * args.list_stride : nullptr;
+                    (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride : nullptr;
                 // kept-block index prefetched one block ahead (off the TMA issue path)
-                int kb_next = (!SDD && lst) ? __ldg(lst) : 0;
+                int kb_next = lst ? __ldg(lst) : 0;
                 int kb = 0;
                 for (int s = 0, li = 0, sub = 0; s < cur.nstages; ++s) {
                     int r0;
-                    if constexpr (!SDD) {
+                    if (!sdd) {
                         if (sub == 0) {
                             kb = lst ? kb_next : li;
                             if (lst && li + 1 < cur.nstages / spb) kb_next = __ldg(lst + li + 1);
                         }
-                        r0 = kb * args.red_blk + sub * kBK;
+                        r0 = kb * a.red_blk + sub * kBK;
                         if (++sub == spb) {
                             sub = 0;
                             ++li;
@@ -247,38 +367,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         r0 = s * kBK;
                     }
-                    ptx::mbar_wait(empty_bar + stage, phase ^ 1);
+                    SD_TWAIT(0, ptx::mbar_wait(empty_bar + stage, phase ^ 1));
                     uint64_t* fb = full_bar + stage;
                     ptx::mbar_arrive_expect_tx(fb, tx_bytes);
                     uint8_t* sA = smem + kOffA + stage * kABytes;
                     uint8_t* sB = smem + kOffB + stage * kBBytes;
-                    if constexpr (!A_MN) {
-                        ptx::tma_load_2d(&tmA, fb, sA, r0, cur.row0, pol);
+                    if (!a_mn) {
+                        ptx::tma_load_2d(tmA, fb, sA, r0, cur.row0, pol);
                     } else {
-                        ptx::tma_load_2d(&tmA, fb, sA, cur.row0, r0, pol);
-                        ptx::tma_load_2d(&tmA, fb, sA + 8192, cur.row0 + 64, r0, pol);
+                        ptx::tma_load_2d(tmA, fb, sA, cur.row0, r0, pol);
+                        ptx::tma_load_2d(tmA, fb, sA + 8192, cur.row0 + 64, r0, pol);
                     }
-                    if constexpr (!SDD) {
-                        if constexpr (!B_MN) {
+                    if (!sdd) {
+                        if (!b_mn) {
                             for (int j = 0; j < cur.n_eff / 128; ++j)
-                                ptx::tma_load_2d(&tmB, fb, sB + j * 16384, r0, cur.n0 + 128 * j, pol);
+                                ptx::tma_load_2d(tmB, fb, sB + j * 16384, r0, cur.n0 + 128 * j, pol);
                         } else {
                             for (int j = 0; j < cur.n_eff / 64; ++j)
-                                ptx::tma_load_2d(&tmB, fb, sB + j * 8192, cur.n0 + 64 * j, r0, pol);
+                                ptx::tma_load_2d(tmB, fb, sB + j * 8192, cur.n0 + 64 * j, r0, pol);
                         }
                     } else {
                         for (int sl = 0; sl < cur.nslots; ++sl) {
-                            const int col0 = cur.slot_blk[sl] * args.out_col_blk;
-                            if constexpr (!B_MN) {
-                                const int per = args.out_col_blk / 128;
+                            const int col0 = cur.slot_blk[sl] * a.out_col_blk;
+                            if (!b_mn) {
+                                const int per = a.out_col_blk / 128;
                                 for (int j = 0; j < per; ++j)
-                                    ptx::tma_load_2d(&tmB, fb, sB + (sl * per + j) * 16384, r0,
-                                                     col0 + 128 * j, pol);
+                                    ptx::tma_load_2d(tmB, fb, sB + (sl * per + j) * 16384, r0, col0 + 128 * j, pol);
                             } else {
-                                const int per = args.out_col_blk / 64;
+                                const int per = a.out_col_blk / 64;
                                 for (int j = 0; j < per; ++j)
-                                    ptx::tma_load_2d(&tmB, fb, sB + (sl * per + j) * 8192,
-                                                     col0 + 64 * j, r0, pol);
+                                    ptx::tma_load_2d(tmB, fb, sB + (sl * per + j) * 8192, col0 + 64 * j, r0, pol);
                             }
                         }
                     }
@@ -298,33 +416,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             int sslot = 0;
             uint32_t sphase = 0;
             while (true) {
-                ptx::mbar_wait(sfull_bar + sslot, sphase);
+                SD_TWAIT(4, ptx::mbar_wait(sfull_bar + sslot, sphase));
                 const Unit t = sched_unit[sslot];
                 ptx::mbar_arrive(sempty_bar + sslot);
                 if (++sslot == kSchedDepth) {
                     sslot = 0;
                     sphase ^= 1;
                 }
-                if (t.row0 < 0) break;
+                if (t.prob < 0) break;
                 if (t.n_eff == 0) continue;
+                const GemmArgs& a = L.p[t.prob];
+                const bool a_mn = a.flags & kFlagAMN;
+                const bool b_mn = a.flags & kFlagBMN;
                 const uint32_t acc = acc_iter & 1;
                 const uint32_t acc_phase = (acc_iter >> 1) & 1;
                 ++acc_iter;
-                ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1);
+                SD_TWAIT(3, ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1));
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
-                const uint32_t idesc = ptx::make_idesc_bf16(kBM, t.n_eff, A_MN, B_MN);
+                const uint32_t idesc = ptx::make_idesc_bf16(kBM, t.n_eff, a_mn, b_mn);
+                const uint32_t a_step = a_mn ? 2048u : 32u, b_step = b_mn ? 2048u : 32u;
+                const uint32_t a_lbo = a_mn ? 8192u : 0u, b_lbo = b_mn ? 8192u : 0u;
                 for (int s = 0; s < t.nstages; ++s) {
-                    ptx::mbar_wait(full_bar + stage, phase);
+                    SD_TWAIT(2, ptx::mbar_wait(full_bar + stage, phase));
+                    SD_TADD(8, 1);
                     ptx::tc_fence_after();
                     const uint32_t a_addr = sbase + kOffA + stage * kABytes;
                     const uint32_t b_addr = sbase + kOffB + stage * kBBytes;
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t ad = A_MN ? ptx::make_sw128_desc(a_addr + k * 2048, 8192, 1024)
-                                                 : ptx::make_sw128_desc(a_addr + k * 32, 0, 1024);
-                        const uint64_t bd = B_MN ? ptx::make_sw128_desc(b_addr + k * 2048, 8192, 1024)
-                                                 : ptx::make_sw128_desc(b_addr + k * 32, 0, 1024);
+                        const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                        const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
                         ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(empty_bar + stage);
@@ -334,8 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 ptx::mma_commit(tfull_bar + acc);
-                if (args.counters)
-                    atomicAdd(args.counters + t.row0 / kBM,
+                if (a.counters)
+                    atomicAdd(a.counters + t.row0 / kBM,
                               static_cast<unsigned long long>(t.nstages / 2) * (t.n_eff / 128));
             }
         }
@@ -346,11 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ebuf_addr = sbase + kOffEpi + q * 2 * kEpiBufBytes;
         uint32_t bi = 0;
         uint32_t acc_iter = 0;
-        constexpr int kChunkCols = OUT_F32 ? 32 : 64;  // 128 bytes of output per row
         int sslot = 0;
         uint32_t sphase = 0;
         while (true) {
-            ptx::mbar_wait(sfull_bar + sslot, sphase);
+            SD_TWAIT(6, ptx::mbar_wait(sfull_bar + sslot, sphase));
             const Unit t = sched_unit[sslot];
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(sempty_bar + sslot);
@@ -358,79 +479,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sslot = 0;
                 sphase ^= 1;
             }
-            if (t.row0 < 0) break;
-            const int row_first = t.row0 + 32 * q;
-            if constexpr (SDD) {
-                for (int z = 0; z < t.nzero; ++z)
-                    zero_rows<OUT_F32>(args, row_first, t.zero_blk[z] * args.out_col_blk,
-                                       args.out_col_blk, lane);
-            }
-            if (t.n_eff == 0) {
-                if constexpr (!SDD) {
-                    const int rem = args.cols_out - t.n0;
-                    zero_rows<OUT_F32>(args, row_first, t.n0, rem < kBN ? rem : kBN, lane);
-                }
-                continue;
-            }
-            const uint32_t acc = acc_iter & 1;
-            const uint32_t acc_phase = (acc_iter >> 1) & 1;
-            ++acc_iter;
-            ptx::mbar_wait(tfull_bar + acc, acc_phase);
-            ptx::tc_fence_after();
-            const int nchunks = t.n_eff / kChunkCols;
-            for (int c = 0; c < nchunks; ++c) {
-                const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kBN + c * kChunkCols;
-                uint32_t v[kChunkCols];
-                ptx::tmem_ld_32x32b_x32(taddr, v);
-                if constexpr (!OUT_F32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
-                ptx::tmem_ld_wait();
-                if (c == nchunks - 1) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(tempty_bar + acc);
-                }
-                // staging buffer bi must no longer be read by the TMA store issued 2 chunks ago
-                if (lane == 0) ptx::bulk_wait_group_read<1>();
-                __syncwarp();
-                const uint32_t row_addr = ebuf_addr + bi * kEpiBufBytes + lane * 128;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    uint32_t w0, w1, w2, w3;
-                    if constexpr (OUT_F32) {
-                        w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * args.scale);
-                        w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * args.scale);
-                        w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * args.scale);
-                        w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * args.scale);
-                    } else {
-                        const float* f = reinterpret_cast<const float*>(v) + 8 * j;
-                        w0 = ptx::pack_bf16x2(f[0] * args.scale, f[1] * args.scale);
-                        w1 = ptx::pack_bf16x2(f[2] * args.scale, f[3] * args.scale);
-                        w2 = ptx::pack_bf16x2(f[4] * args.scale, f[5] * args.scale);
-                        w3 = ptx::pack_bf16x2(f[6] * args.scale, f[7] * args.scale);
-                    }
-                    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), w0, w1, w2, w3);
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    int col;
-                    if constexpr (SDD) {
-                        const int tcol = c * kChunkCols;
-                        const int sl = tcol / args.out_col_blk;
-                        col = t.slot_blk[sl] * args.out_col_blk + (tcol - sl * args.out_col_blk);
-                    } else {
-                        col = t.n0 + c * kChunkCols;
-                    }
-                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
-                    ptx::bulk_commit_group();
-                }
-                bi ^= 1;
-            }
+            if (t.prob < 0) break;
+            const GemmArgs& a = L.p[t.prob];
+            const CUtensorMap* tmOut = &tms.m[3 * t.prob + 2];
+            if (a.flags & kFlagF32)
+                epilogue_unit<true>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr, bi,
+                                    acc_iter, tr);
+            else
+                epilogue_unit<false>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr, bi,
+                                     acc_iter, tr);
+            SD_TADD(11, 1);
         }
         if (lane == 0) ptx::bulk_wait_group<0>();
         __syncwarp();
     }
 
+#ifdef SD_TRACE
+    {
+        const long long t_role_end = clock64();
+        // warp 0 lane 0 (producer) -> slots 0,1,9 ; warp 1 lane 0 (MMA) -> 2,3,4,7,8 ; warp 4 lane 0 -> 5,6,10,11
+        unsigned long long* out = g_sd_trace + blockIdx.x * kTraceSlots;
+        if (warp == 0 && lane == 0) {
+            atomicAdd(out + 0, tr[0]); atomicAdd(out + 1, tr[1]); atomicAdd(out + 9, t_role_end - t_start);
+        } else if (warp == 1 && lane == 0) {
+            atomicAdd(out + 2, tr[2]); atomicAdd(out + 3, tr[3]); atomicAdd(out + 4, tr[4]);
+            atomicAdd(out + 7, t_role_end - t_start); atomicAdd(out + 8, tr[8]);
+        } else if (warp == 4 && lane == 0) {
+            atomicAdd(out + 5, tr[5]); atomicAdd(out + 6, tr[6]); atomicAdd(out + 10, t_role_end - t_start);
+            atomicAdd(out + 11, tr[11]);
+        }
+    }
+#else
+    (void)tr;
+#endif
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -438,29 +519,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         // last CTA out re-arms the scheduler slot for the next launch
         __threadfence();
-        if (atomicAdd(args.sched + 1, 1u) == gridDim.x - 1) {
-            args.sched[0] = 0u;
-            args.sched[1] = 0u;
+        if (atomicAdd(L.sched + 1, 1u) == gridDim.x - 1) {
+            L.sched[0] = 0u;
+            L.sched[1] = 0u;
             __threadfence();
         }
     }
 }
 
-template <bool A_MN, bool B_MN, bool SDD, bool OUT_F32>
-void launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout,
-                 const GemmArgs& args, cudaStream_t s) {
-    auto kern = sd_gemm_kernel<A_MN, B_MN, SDD, OUT_F32>;
-    static bool configured = false;  // per instantiation; attribute is per-function
+}  // namespace
+
+void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
+    if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
+    static bool configured = false;
     if (!configured) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes),
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes),
                    "cudaFuncSetAttribute(max dynamic smem)");
         configured = true;
     }
-    const int units = args.n_row_tiles * args.n_col_units;
-    const int grid = units < num_sms() ? units : num_sms();
+    TensorMaps tms;
+    LaunchArgs L;
+    std::memset(&L, 0, sizeof L);
+    int total = 0;
+    for (int i = 0; i < n; ++i) {
+        tms.m[3 * i] = calls[i]->ta;
+        tms.m[3 * i + 1] = calls[i]->tb;
+        tms.m[3 * i + 2] = calls[i]->tout;
+        L.p[i] = calls[i]->args;
+        L.p[i].unit_begin = total;
+        L.p[i].num_units = L.p[i].n_row_tiles * L.p[i].n_col_units;
+        total += L.p[i].num_units;
+    }
+    for (int i = n; i < kMaxProblems; ++i) tms.m[3 * i] = tms.m[3 * i + 1] = tms.m[3 * i + 2] = tms.m[0];
+    L.nprob = n;
+    L.total_units = total;
+    const int grid = total < num_sms() ? total : num_sms();
     if (grid <= 0) return;
-    GemmArgs a = args;
-    a.sched = sched_slot();
+    L.sched = sched_slot();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -471,37 +566,18 @@ void launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, tout, a), "sd_gemm_kernel launch");
-    check_cuda(cudaGetLastError(), "sd_gemm_kernel launch");
+    check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel, tms, L), "sd_gemm_kernel launch");
     note_launch();
 }
 
-}  // namespace
-
-void launch_gemm(bool a_mn, bool b_mn, GemmKind kind, bool out_f32, const CUtensorMap& ta,
-                 const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& args,
-                 cudaStream_t s) {
-    const bool sdd = kind == GemmKind::sdd;
-#define SD_DISPATCH(AM, BM_, SD_, F32)                                                    \
-    if (a_mn == AM && b_mn == BM_ && sdd == SD_ && out_f32 == F32)                        \
-        return launch_impl<AM, BM_, SD_, F32>(ta, tb, tout, args, s);
-    // dsd / dense forward (X K-major, W MN-major)
-    SD_DISPATCH(false, true, false, false)
-    SD_DISPATCH(false, true, false, true)
-    // dsd dW (X^T MN-major, dY MN-major) and dense x^T dy
-    SD_DISPATCH(true, true, false, false)
-    SD_DISPATCH(true, true, false, true)
-    // dense dy W^T (both K-major)
-    SD_DISPATCH(false, false, false, false)
-    SD_DISPATCH(false, false, false, true)
-    // sdd dX in the layer (dY K-major, W K-major)
-    SD_DISPATCH(false, false, true, false)
-    SD_DISPATCH(false, false, true, true)
-    // sdd reference form (a K-major, b row-major = MN-major)
-    SD_DISPATCH(false, true, true, false)
-    SD_DISPATCH(false, true, true, true)
-#undef SD_DISPATCH
-    fail(SD_EINVAL, "unsupported GEMM operand layout combination");
-}
-
 }  // namespace sd
+
+#ifdef SD_TRACE
+extern "C" SD_API int sd_trace_read(unsigned long long* host, int n) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return SD_ERUNTIME;
+    if (cudaMemcpyFromSymbol(host, g_sd_trace, sizeof(unsigned long long) * n) != cudaSuccess) return SD_ERUNTIME;
+    static unsigned long long zeros[1024 * kTraceSlots] = {0};
+    cudaMemcpyToSymbol(g_sd_trace, zeros, sizeof zeros);
+    return SD_OK;
+}
+#endif

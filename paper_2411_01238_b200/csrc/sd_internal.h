@@ -36,40 +36,56 @@ constexpr int kBM = 128;
 constexpr int kBN = 256;
 constexpr int kBK = 64;
 
+// Operand / output layout flags of one GEMM problem.
+enum GemmFlags : uint32_t {
+    kFlagAMN = 1u,  // A is MN-major (contiguous along the output rows), else K-major
+    kFlagBMN = 2u,  // B is MN-major (contiguous along the output columns), else K-major
+    kFlagSDD = 4u,  // output-block skipping (sdd) instead of reduction-block skipping (dsd)
+    kFlagF32 = 8u,  // fp32 output, else bf16
+};
+
 struct GemmArgs {
+    uint32_t flags;    // GemmFlags
     int rows_out;      // output rows (multiple of 128)
     int cols_out;      // output columns (multiple of 128)
     int red;           // reduction length (multiple of 64)
     int n_row_tiles;   // rows_out / 128
     int n_col_units;   // ceil(cols_out / 256)
     // dsd: per output-row-block list of kept reduction blocks (null = dense)
+    // sdd: per output-row-block list of kept output blocks (+ dropped at the tail)
     const int32_t* list_cnt;
     const int32_t* list_idx;
     int list_stride;
     int red_blk;       // reduction block (mask block along the reduction), multiple of 64
     int out_row_blk;   // output rows per list/mask row (multiple of 128)
     const int32_t* row_order;  // optional tile-row permutation (when out_row_blk == 128)
-    // sdd: output-block mask bits
-    const uint64_t* words;
-    int mask_cols;     // mask block columns (output column blocks)
-    int out_col_blk;   // output column block (128 or 256)
+    const uint64_t* words;     // mask bits (informational)
+    int mask_cols;     // mask block columns (sdd: output column blocks)
+    int out_col_blk;   // sdd output column block (128 or 256)
     float scale;
     void* out;
     unsigned long long* counters;
-    unsigned int* sched;  // {next-unit counter, CTAs-done counter}, zero between launches
+    int unit_begin;    // filled by launch_gemms: first global unit of this problem
+    int num_units;     // filled by launch_gemms
 };
 
 // A zeroed {counter, done} pair for one persistent-kernel launch (ring of
 // slots per device, re-armed by the last CTA of the launch that used it).
 unsigned int* sched_slot();
 
-// A_MN / B_MN: operand is MN-major (contiguous along the output dimension)
-// rather than K-major (contiguous along the reduction).
-enum class GemmKind { dsd, sdd };
+// A fully validated, ready-to-launch GEMM problem (tensor maps encoded).
+struct GemmCall {
+    CUtensorMap ta, tb, tout;
+    GemmArgs args;
+};
 
-void launch_gemm(bool a_mn, bool b_mn, GemmKind kind, bool out_f32, const CUtensorMap& ta,
-                 const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& args,
-                 cudaStream_t s);
+// Launch 1 or 2 independent GEMM problems as ONE persistent kernel sharing a
+// single heaviest-first work queue (problem 0's units are handed out first).
+void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s);
+inline void launch_gemm(const GemmCall& c, cudaStream_t s) {
+    const GemmCall* p = &c;
+    launch_gemms(&p, 1, s);
+}
 
 // 2D row-major tensor map: `inner` contiguous elements, `outer` rows, 128B swizzle.
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,
