@@ -34,6 +34,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "sd_internal.h"
@@ -369,6 +371,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     SD_TWAIT(0, ptx::mbar_wait(empty_bar + stage, phase ^ 1));
                     uint64_t* fb = full_bar + stage;
+#ifdef SD_DIAG_NO_TMA
+                    ptx::mbar_arrive(fb);
+                    (void)tx_bytes;
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+#endif
                     ptx::mbar_arrive_expect_tx(fb, tx_bytes);
                     uint8_t* sA = smem + kOffA + stage * kABytes;
                     uint8_t* sB = smem + kOffB + stage * kBBytes;
@@ -443,12 +454,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a_addr = sbase + kOffA + stage * kABytes;
                     const uint32_t b_addr = sbase + kOffB + stage * kBBytes;
+#ifndef SD_DIAG_NO_MMA
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
                         const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
                         const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
                         ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
                     }
+#else
+                    (void)a_addr; (void)b_addr; (void)idesc; (void)a_step; (void)b_step; (void)a_lbo; (void)b_lbo;
+#endif
                     ptx::mma_commit(empty_bar + stage);
                     if (++stage == kStages) {
                         stage = 0;
@@ -553,7 +568,11 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     for (int i = n; i < kMaxProblems; ++i) tms.m[3 * i] = tms.m[3 * i + 1] = tms.m[3 * i + 2] = tms.m[0];
     L.nprob = n;
     L.total_units = total;
-    const int grid = total < num_sms() ? total : num_sms();
+    int cap = num_sms();
+#ifdef SD_TRACE
+    if (const char* e = std::getenv("SD_MAX_CTAS")) cap = std::max(1, std::min(cap, std::atoi(e)));
+#endif
+    const int grid = total < cap ? total : cap;
     if (grid <= 0) return;
     L.sched = sched_slot();
     cudaLaunchConfig_t cfg = {};
