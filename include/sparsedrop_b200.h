@@ -188,6 +188,12 @@ SD_API int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream);
 SD_API int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream);
 SD_API int sd_layer_plan_destroy(sd_layer_plan* plan);
 
+/* The MLP block's activation between two SparseDrop Linears (configs[2]):
+ * exact GELU and its backward, one HBM pass each over n bf16 values
+ * (n % 8 == 0, 16-byte aligned). act = h*Phi(h); dh = grad*(Phi(h) + h*phi(h)). */
+SD_API int sd_gelu_forward(const void* h, void* act, int64_t n, void* stream);
+SD_API int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void* stream);
+
 /* Effective FLOPs (gemm.hpp:217-228): kind 0 = dsd (2*n*m_blk*k_blk*keep),
  * 1 = sdd (2*k*m_blk*n_blk*keep). */
 SD_API uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k);

@@ -78,6 +78,8 @@ PROTOTYPES = {
     "sd_layer_plan_dense_forward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
+    "sd_gelu_forward": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
+    "sd_gelu_backward": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P]),
     "sd_flops_dense": (ctypes.c_uint64, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]),
     "sd_flops_effective": (
         ctypes.c_uint64,

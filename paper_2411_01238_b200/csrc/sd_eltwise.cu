@@ -1,0 +1,108 @@
+// sd_eltwise.cu — the MLP block's activation between the two SparseDrop
+// Linears (configs[2]): GELU forward and its backward, each ONE
+// HBM pass over bf16 data (16-byte vectors, grid = multiple of the SM count).
+// Exact (erf) GELU, fp32 math: act = h * Phi(h);  dh = g * (Phi(h) + h * phi(h)).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "sd_internal.h"
+
+namespace sd {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float phi_cdf(float x) { return 0.5f * (1.0f + erff(x * 0.70710678118654752f)); }
+
+__device__ __forceinline__ uint4 ld_nc(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(b[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) gelu_fwd_kernel(const uint4* __restrict__ h, uint4* __restrict__ act,
+                                                            int64_t n8) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        float x[8];
+        unpack8(ld_nc(h + i), x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = x[j] * phi_cdf(x[j]);
+        act[i] = pack8(x);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) gelu_bwd_kernel(const uint4* __restrict__ h, const uint4* __restrict__ g,
+                                                            uint4* __restrict__ dh, int64_t n8) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        float x[8], gr[8];
+        unpack8(ld_nc(h + i), x);
+        unpack8(ld_nc(g + i), gr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float pdf = 0.3989422804014327f * __expf(-0.5f * x[j] * x[j]);
+            gr[j] = gr[j] * (phi_cdf(x[j]) + x[j] * pdf);
+        }
+        dh[i] = pack8(gr);
+    }
+}
+
+int grid_for(int64_t n8) {
+    const int64_t blocks = (n8 + kThreads - 1) / kThreads;
+    const int cap = num_sms() * 8;
+    return static_cast<int>(blocks < cap ? blocks : cap);
+}
+
+}  // namespace
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+SD_API int sd_gelu_forward(const void* h, void* act, int64_t n, void* stream);
+SD_API int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void* stream);
+
+int sd_gelu_forward(const void* h, void* act, int64_t n, void* stream) {
+    if (!h || !act || n < 0 || n % 8 || reinterpret_cast<uintptr_t>(h) % 16 || reinterpret_cast<uintptr_t>(act) % 16)
+        return SD_EINVAL;
+    if (n == 0) return SD_OK;
+    gelu_fwd_kernel<<<grid_for(n / 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(h), static_cast<uint4*>(act), n / 8);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? SD_OK : SD_ERUNTIME;
+}
+
+int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void* stream) {
+    if (!h || !grad || !dh || n < 0 || n % 8 || reinterpret_cast<uintptr_t>(h) % 16 ||
+        reinterpret_cast<uintptr_t>(grad) % 16 || reinterpret_cast<uintptr_t>(dh) % 16)
+        return SD_EINVAL;
+    if (n == 0) return SD_OK;
+    gelu_bwd_kernel<<<grid_for(n / 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(h), static_cast<const uint4*>(grad), static_cast<uint4*>(dh), n / 8);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? SD_OK : SD_ERUNTIME;
+}
+
+}  // extern "C"

@@ -455,3 +455,64 @@ def test_native_library_loaded(sd):
     assert sd.launch_count() == n0 + 1
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libsparsedrop_b200.so" in maps
+
+
+def test_mlp_block_composition(sd, oracle):
+    """ViT-style MLP block (cfg3 shape family): each stage vs the oracle on the
+    same bf16 intermediates, masks from effective_seed(seed, step, layer)."""
+    from paper_2411_01238_b200.mlp import SparseDropMLP, gelu_grad, gelu_grad_reference, gelu_reference
+
+    M, D, H, p = 1024, 256, 768, 0.5
+    x, w1, w2, dy = _dev(oracle, M, D, 1), _dev(oracle, D, H, 2), _dev(oracle, H, D, 3), _dev(oracle, M, D, 4)
+    mlp = SparseDropMLP(x, w1, w2, dy, p, seed=5)
+    y, dx, dw1, dw2 = mlp.step(step_seed=9)
+    torch.cuda.synchronize()
+    s = sd.dropout_scale(p)
+    w0, _ = oracle.sample_mask(p, 128, 128, oracle.effective_seed(5, 9, 0), M, D)
+    w1m, _ = oracle.sample_mask(p, 128, 128, oracle.effective_seed(5, 9, 1), M, H)
+    assert np.array_equal(words_np(mlp.fc1.mask), w0) and np.array_equal(words_np(mlp.fc2.mask), w1m)
+    xn, w1n, w2n, dyn = _np(x), _np(w1), _np(w2), _np(dy)
+    h = mlp.fc1.y
+    check_bf16(_np(h), oracle.dsd_matmul(xn, w0, w1n, 128, 128, 128, s), s * _abs_prod(np.abs(xn), np.abs(w1n)))
+    act = _np(mlp.act)
+    # the fused activation kernels vs the torch fp32 reference (bf16 outputs: 1 ulp)
+    assert (mlp.act.float() - gelu_reference(h).float()).abs().max().item() <= 2**-7 * (
+        gelu_reference(h).float().abs().max().item())
+    gref = gelu_grad_reference(h, mlp.fc2.dx).float()
+    assert ((mlp.dact.float() - gref).abs() <= 2**-7 * gref.abs() + 1e-6).all()
+    check_bf16(_np(y), oracle.dsd_matmul(act, w1m, w2n, 128, 128, 128, s), s * _abs_prod(np.abs(act), np.abs(w2n)))
+    check_f32(_np(dw2), oracle.layer_dw(act, dyn, w1m, 128, 128, s), s * _abs_prod(np.abs(act).T, np.abs(dyn)))
+    da_ref = oracle.layer_dx(dyn, w2n, w1m, 128, 128, s)
+    check_bf16(_np(mlp.fc2.dx), da_ref, s * _abs_prod(np.abs(dyn), np.abs(w2n).T))
+    dact = _np(mlp.dact)
+    assert torch.equal(mlp.dact, gelu_grad(h, mlp.fc2.dx))
+    check_f32(_np(dw1), oracle.layer_dw(xn, dact, w0, 128, 128, s), s * _abs_prod(np.abs(xn).T, np.abs(dact)))
+    check_bf16(_np(dx), oracle.layer_dx(dact, w1n, w0, 128, 128, s), s * _abs_prod(np.abs(dact), np.abs(w1n).T))
+
+
+def test_cfg4_sampled_rows(sd, oracle):
+    """configs[3] size (M=65536, K=N=8192, p=0.3): sampled row blocks of Y and dX."""
+    M, N, K, p = 65536, 8192, 8192, 0.3
+    x, w, dy = _dev(oracle, 1024, K, 1), _dev(oracle, K, N, 2), _dev(oracle, 1024, N, 3)
+    # tile the 1024-row generated blocks to full size (the oracle only needs the sampled rows)
+    x = x.repeat(M // 1024, 1)
+    dy = dy.repeat(M // 1024, 1)
+    plan = sd.LayerPlan(x, w, dy, p)
+    plan.forward(seed=0)
+    plan.backward()
+    torch.cuda.synchronize()
+    words = words_np(plan.mask)
+    wo, keep = oracle.sample_mask(p, 128, 128, 0, M, K)
+    assert np.array_equal(words, wo) and plan.mask.keep_count() == keep == 22942
+    s = sd.dropout_scale(p)
+    wn = _np(w)
+    for r in [0, 301]:
+        lo, hi = r * 128, (r + 1) * 128
+        xs, dys = _np(x[lo:hi]), _np(dy[lo:hi])
+        # the oracle wants full matrices; pass the slab with a slab-local mask row
+        rw, _ = oracle.sample_mask(p, 128, 128, 0, 128, K, row_block_offset=r)
+        ref_y = oracle.dsd_matmul(xs, rw, wn, 128, 128, 128, s)
+        check_bf16(_np(plan.y[lo:hi]), ref_y, s * _abs_prod(np.abs(xs), np.abs(wn)))
+        ref_dx = oracle.layer_dx(dys, wn, rw, 128, 128, s)
+        check_bf16(_np(plan.dx[lo:hi]), ref_dx, s * _abs_prod(np.abs(dys), np.abs(wn).T))
+        assert np.array_equal(_np(plan.dx[lo:hi]) == 0, ref_dx == 0)

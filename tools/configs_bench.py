@@ -1,0 +1,126 @@
+"""Every BASELINE.json configuration on one B200 (bench.py measures configs[1]).
+
+  python tools/configs_bench.py [--out gpurun_out/configs.json] [--quick]
+
+cfg1  SparseDrop layer fwd+bwd 1024^3, p=0.5
+cfg3  ViT-B MLP training step, 65536 tokens, 768 -> 3072 -> 768, SparseDrop
+      before each Linear (GELU between), p=0.1/0.5, vs the same step dense
+cfg4  LLM projection M=65536, K=N=8192, p=0.1/0.3/0.5, vs dense
+cfg5  one GPU's row shard of M=524288, K=N=8192 (the G=1 point), p=0.1/0.5
+Timing: CUDA events per step, L2 flushed between steps, 0.3 s sustained
+pre-roll per configuration (steady power-capped state); dense-equivalent and
+executed TFLOP/s, speed-up vs our dense tcgen05 path on the same buffers.
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_2411_01238_b200 as sd  # noqa: E402
+from paper_2411_01238_b200.mlp import SparseDropMLP  # noqa: E402
+
+dev = torch.device("cuda", 0)
+gen = torch.Generator(device=dev)
+gen.manual_seed(7)
+flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+
+def synth(r, c):
+    u = torch.rand(r, c, generator=gen, device=dev)
+    sign = torch.where(torch.rand(r, c, generator=gen, device=dev) < 0.5, -1.0, 1.0)
+    return ((0.25 + u) * sign).to(torch.bfloat16)
+
+
+def timed(step, steps, preroll_s=0.3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for j in range(2):
+        step(j)
+    torch.cuda.synchronize()
+    est = max((time.perf_counter() - t0) / 2, 1e-5)
+    for j in range(int(min(max(preroll_s / est, 1), 5000))):
+        step(j)
+    torch.cuda.synchronize()
+    tot = 0.0
+    for i in range(steps):
+        flush_buf.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step(100 + i)
+        b.record()
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    return tot / steps
+
+
+def layer_cfg(name, M, N, K, ps, steps):
+    x, w, dy = synth(M, K), synth(K, N), synth(M, N)
+    out = []
+    dense_ms = None
+    flops = 3 * 2 * M * N * K
+    for p in ps:
+        plan = sd.LayerPlan(x, w, dy, p)
+        ms = timed(lambda i: (plan.forward(sd.effective_seed(0, i, 0)), plan.backward()), steps)
+        keep = plan.mask.keep_count() / plan.mask.total_blocks()
+        if dense_ms is None:
+            dense_ms = timed(lambda i: (plan.dense_forward(), plan.dense_backward()), steps)
+        out.append({"config": name, "M": M, "N": N, "K": K, "p": p, "keep": keep, "ms_per_step": ms,
+                    "dense_ms_per_step": dense_ms, "speedup_vs_dense": dense_ms / ms,
+                    "dense_equiv_tflops": flops / (ms * 1e-3) / 1e12,
+                    "executed_tflops": keep * flops / (ms * 1e-3) / 1e12,
+                    "dense_tflops": flops / (dense_ms * 1e-3) / 1e12})
+        print(json.dumps(out[-1]), flush=True)
+        del plan
+    del x, w, dy
+    torch.cuda.empty_cache()
+    return out
+
+
+def mlp_cfg(ps, steps):
+    M, D, H = 65536, 768, 3072
+    x, w1, w2, dy = synth(M, D), synth(D, H), synth(H, D), synth(M, D)
+    flops = 2 * (3 * 2 * M * D * H)  # two Linears, fwd + bwd (GELU not counted)
+    dense = SparseDropMLP(x, w1, w2, dy, 0.0, dense=True)
+    dense_ms = timed(lambda i: dense.step(i), steps)
+    del dense
+    out = []
+    for p in ps:
+        mlp = SparseDropMLP(x, w1, w2, dy, p)
+        ms = timed(lambda i: mlp.step(i), steps)
+        k1 = mlp.fc1.mask.keep_count() / mlp.fc1.mask.total_blocks()
+        k2 = mlp.fc2.mask.keep_count() / mlp.fc2.mask.total_blocks()
+        keep = (k1 + k2) / 2
+        out.append({"config": "cfg3_vit_b_mlp", "tokens": M, "dims": [D, H, D], "p": p, "keep_fc1": k1,
+                    "keep_fc2": k2, "ms_per_step": ms, "dense_ms_per_step": dense_ms,
+                    "speedup_vs_dense": dense_ms / ms, "dense_equiv_tflops": flops / (ms * 1e-3) / 1e12,
+                    "executed_tflops": keep * flops / (ms * 1e-3) / 1e12,
+                    "note": "GELU/GELU' are torch elementwise ops inside the timed step"})
+        print(json.dumps(out[-1]), flush=True)
+        del mlp
+    del x, w1, w2, dy
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.json"))
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    res = []
+    res += layer_cfg("cfg1", 1024, 1024, 1024, [0.5], 20)
+    res += mlp_cfg([0.1, 0.5], 5 if args.quick else 10)
+    res += layer_cfg("cfg4", 65536, 8192, 8192, [0.1, 0.3, 0.5], 3 if args.quick else 5)
+    if not args.quick:
+        res += layer_cfg("cfg5_G1_shard", 524288, 8192, 8192, [0.1, 0.5], 3)
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
