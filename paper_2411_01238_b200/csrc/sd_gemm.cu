@@ -91,7 +91,7 @@ struct Unit {
     int slot_blk[2];
     int nzero;     // sdd: dropped output blocks in this unit
     int zero_blk[2];
-    int pad[4];
+    int pad[4];    // pad[0]: dsd first list entry of this unit (split-K)
 };
 static_assert(sizeof(Unit) == 64, "Unit layout");
 
@@ -112,6 +112,10 @@ struct TensorMaps {
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) {
     Unit t;
     t.prob = prob;
+    // split-K (dsd only): the split index is the outermost coordinate
+    const int base_units = a.n_row_tiles * a.n_col_units;
+    const int split = u / base_units;
+    u -= split * base_units;
     // Grouped rasterization: tile rows (sorted heaviest first) are taken in
     // groups of kGroupRows; inside a group units go column-unit-major. The
     // CTAs in flight then share a few operand column/row slabs (L2 reuse), heavy
@@ -133,8 +137,12 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         const int rem = a.cols_out - t.n0;
         t.n_eff = rem < kBN ? rem : kBN;
         const int cnt = a.list_cnt ? __ldg(a.list_cnt + t.list_row) : a.red / a.red_blk;
-        t.nstages = cnt * (a.red_blk / kBK);
-        if (cnt == 0) t.n_eff = 0;
+        // this split's contiguous share [lo, hi) of the row's kept blocks
+        const int lo = static_cast<int>((static_cast<int64_t>(cnt) * split) / a.splits);
+        const int hi = static_cast<int>((static_cast<int64_t>(cnt) * (split + 1)) / a.splits);
+        t.pad[0] = lo;  // first list entry
+        t.nstages = (hi - lo) * (a.red_blk / kBK);
+        if (hi == lo) t.n_eff = 0;
     } else {
         // Pack the row's KEPT output blocks (compacted list, ascending) into
         // 256-wide units, so every unit but the row's last runs a full N=256 MMA;
@@ -193,7 +201,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
             zero_rows<OUT_F32>(a, row_first, t.zero_blk[z] * a.out_col_blk, a.out_col_blk, lane);
     }
     if (t.n_eff == 0) {
-        if (!sdd) {
+        if (!sdd && !(a.flags & kFlagReduce)) {
             const int rem = a.cols_out - t.n0;
             zero_rows<OUT_F32>(a, row_first, t.n0, rem < kBN ? rem : kBN, lane);
         }
@@ -248,7 +256,10 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
             } else {
                 col = t.n0 + c * kChunkCols;
             }
-            ptx::tma_store_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
+            if (a.flags & kFlagReduce)
+                ptx::tma_reduce_add_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
+            else
+                ptx::tma_store_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
             ptx::bulk_commit_group();
         }
         bi ^= 1;
@@ -349,8 +360,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool sdd = a.flags & kFlagSDD;
                 const uint32_t tx_bytes = kABytes + cur.n_eff * kBK * 2;
                 const int spb = a.red_blk / kBK;
+                const int li0 = sdd ? 0 : cur.pad[0];
                 const int32_t* lst =
-                    (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride : nullptr;
+                    (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
+                                         : nullptr;
                 // kept-block index prefetched one block ahead (off the TMA issue path)
                 int kb_next = lst ? __ldg(lst) : 0;
                 int kb = 0;
@@ -358,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int r0;
                     if (!sdd) {
                         if (sub == 0) {
-                            kb = lst ? kb_next : li;
+                            kb = lst ? kb_next : li0 + li;
                             if (lst && li + 1 < cur.nstages / spb) kb_next = __ldg(lst + li + 1);
                         }
                         r0 = kb * a.red_blk + sub * kBK;
@@ -555,20 +568,53 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     TensorMaps tms;
     LaunchArgs L;
     std::memset(&L, 0, sizeof L);
-    int total = 0;
+    const int sms = num_sms();
+    // split-K for dsd problems with too few output tiles to fill the GPU (e.g.
+    // the MLP's dW, 72 tiles over a 65536-long reduction): fp32 outputs only,
+    // partial sums reduce-added by TMA into the zeroed output (the summation
+    // order across splits is then not fixed; results stay within tolerance).
+    GemmArgs pa[kMaxProblems];
+    float cost[kMaxProblems];
     for (int i = 0; i < n; ++i) {
-        tms.m[3 * i] = calls[i]->ta;
-        tms.m[3 * i + 1] = calls[i]->tb;
-        tms.m[3 * i + 2] = calls[i]->tout;
-        L.p[i] = calls[i]->args;
-        L.p[i].unit_begin = total;
-        L.p[i].num_units = L.p[i].n_row_tiles * L.p[i].n_col_units;
-        total += L.p[i].num_units;
+        pa[i] = calls[i]->args;
+        pa[i].splits = 1;
+        const int base = pa[i].n_row_tiles * pa[i].n_col_units;
+        const bool sdd = pa[i].flags & kFlagSDD;
+        const int red_stages = pa[i].red / kBK;
+        if (!sdd && (pa[i].flags & kFlagF32) && base < 2 * sms && red_stages >= 64) {
+            int sp = (2 * sms + base - 1) / base;
+            sp = std::min(sp, red_stages / 32);
+            if (sp > 1) {
+                pa[i].splits = sp;
+                pa[i].flags |= kFlagReduce;
+                check_cuda(cudaMemsetAsync(pa[i].out, 0,
+                                           static_cast<size_t>(pa[i].rows_out) * pa[i].cols_out * sizeof(float), s),
+                           "cudaMemsetAsync(split-K output)");
+            }
+        }
+        cost[i] = static_cast<float>(red_stages) / pa[i].splits;  // stages per unit (upper bound)
     }
-    for (int i = n; i < kMaxProblems; ++i) tms.m[3 * i] = tms.m[3 * i + 1] = tms.m[3 * i + 2] = tms.m[0];
+    // one shared queue, heaviest units first: the problem with the larger
+    // per-unit cost is handed out first
+    int order[kMaxProblems] = {0, 1};
+    if (n == 2 && cost[1] > cost[0]) {
+        order[0] = 1;
+        order[1] = 0;
+    }
+    int total = 0;
+    for (int j = 0; j < n; ++j) {
+        const int i = order[j];
+        tms.m[3 * j] = calls[i]->ta;
+        tms.m[3 * j + 1] = calls[i]->tb;
+        tms.m[3 * j + 2] = calls[i]->tout;
+        L.p[j] = pa[i];
+        L.p[j].unit_begin = total;
+        L.p[j].num_units = gemm_units(L.p[j]);
+        total += L.p[j].num_units;
+    }
     L.nprob = n;
     L.total_units = total;
-    int cap = num_sms();
+    int cap = sms;
 #ifdef SD_TRACE
     if (const char* e = std::getenv("SD_MAX_CTAS")) cap = std::max(1, std::min(cap, std::atoi(e)));
 #endif

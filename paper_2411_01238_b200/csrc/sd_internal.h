@@ -42,6 +42,7 @@ enum GemmFlags : uint32_t {
     kFlagBMN = 2u,  // B is MN-major (contiguous along the output columns), else K-major
     kFlagSDD = 4u,  // output-block skipping (sdd) instead of reduction-block skipping (dsd)
     kFlagF32 = 8u,  // fp32 output, else bf16
+    kFlagReduce = 16u,  // split-K: the epilogue reduce-adds into a pre-zeroed fp32 output
 };
 
 struct GemmArgs {
@@ -65,9 +66,12 @@ struct GemmArgs {
     float scale;
     void* out;
     unsigned long long* counters;
+    int splits;        // dsd split-K factor (>= 1): each unit reduces a contiguous 1/splits of its list
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
+
+inline int gemm_units(const GemmArgs& a) { return a.n_row_tiles * a.n_col_units * (a.splits > 0 ? a.splits : 1); }
 
 // A zeroed {counter, done} pair for one persistent-kernel launch (ring of
 // slots per device, re-armed by the last CTA of the launch that used it).

@@ -516,3 +516,23 @@ def test_cfg4_sampled_rows(sd, oracle):
         ref_dx = oracle.layer_dx(dys, wn, rw, 128, 128, s)
         check_bf16(_np(plan.dx[lo:hi]), ref_dx, s * _abs_prod(np.abs(dys), np.abs(wn).T))
         assert np.array_equal(_np(plan.dx[lo:hi]) == 0, ref_dx == 0)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.5])
+def test_layer_dw_split_k(sd, oracle, p):
+    """Few output tiles over a long reduction: split-K with TMA reduce-add (fp32)."""
+    M, N, K = 16384, 512, 256
+    x, dy = _dev(oracle, M, K, 1), _dev(oracle, M, N, 3)
+    m = sd.sample_mask(sd.DropoutSpec(p, 128, 128, 6), M, K)
+    s = sd.dropout_scale(p)
+    dw = torch.full((K, N), float("nan"), dtype=torch.float32, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    sd.api.check(sd.load_library().sd_linear_backward_dw(x.data_ptr(), m.cptr(), dy.data_ptr(), s, dw.data_ptr(),
+                                                         0, M, N, K, st))
+    dwt = torch.empty(K, N, dtype=torch.float32, device="cuda")
+    sd.api.check(sd.load_library().sd_dense_gemm_tn(x.data_ptr(), dy.data_ptr(), dwt.data_ptr(), 0, K, N, M, st))
+    torch.cuda.synchronize()
+    xn, dyn = _np(x), _np(dy)
+    bound = s * _abs_prod(np.abs(xn).T, np.abs(dyn))
+    check_f32(_np(dw), oracle.layer_dw(xn, dyn, words_np(m), 128, 128, s), bound)
+    check_f32(_np(dwt), oracle.dense_gemm(xn.T, dyn), _abs_prod(np.abs(xn).T, np.abs(dyn)))
