@@ -61,7 +61,10 @@ __device__ unsigned long long g_sd_trace[1024 * kTraceSlots];
 namespace sd {
 namespace {
 
-constexpr int kStages = 4;
+#ifndef SD_STAGES
+#define SD_STAGES 4
+#endif
+constexpr int kStages = SD_STAGES;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 constexpr int kBBytes = kBN * kBK * 2;  // 32 KB per stage
 constexpr int kEpiWarps = 4;

@@ -36,6 +36,8 @@ dw = torch.empty(K, N, device="cuda", dtype=torch.float32)
 st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
 fns = {
     "dense_nn": lambda: lib.sd_dense_gemm(x.data_ptr(), w.data_ptr(), y.data_ptr(), 1, M, N, K, st()),
+    "dense_nt": lambda: lib.sd_dense_gemm_nt(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), 1, M, K, N, st()),
+    "dense_tn": lambda: lib.sd_dense_gemm_tn(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, K, N, M, st()),
     "fwd": lambda: lib.sd_linear_forward(x.data_ptr(), m.cptr(), w.data_ptr(), s, y.data_ptr(), 1, M, N, K, st()),
     "dw": lambda: lib.sd_linear_backward_dw(x.data_ptr(), m.cptr(), dy.data_ptr(), s, dw.data_ptr(), 0, M, N, K, st()),
     "dx": lambda: lib.sd_linear_backward_dx(dy.data_ptr(), w.data_ptr(), m.cptr(), s, dx.data_ptr(), 1, M, N, K, st()),
@@ -44,7 +46,10 @@ fns = {
 buf = np.zeros(1024 * 16, dtype=np.uint64)
 names = ["prod_wait_empty", "prod_wait_sched", "mma_wait_full", "mma_wait_tmem", "mma_wait_sched", "epi_wait_tfull",
          "epi_wait_sched", "mma_run", "stages", "prod_run", "epi_run", "units"]
+only = os.environ.get("ONLY", "").split(",") if os.environ.get("ONLY") else None
 for name, fn in fns.items():
+    if only and name not in only:
+        continue
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
