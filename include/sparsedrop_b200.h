@@ -194,6 +194,19 @@ SD_API int sd_layer_plan_destroy(sd_layer_plan* plan);
 SD_API int sd_gelu_forward(const void* h, void* act, int64_t n, void* stream);
 SD_API int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void* stream);
 
+/* Generic dense tcgen05 GEMM c[m,n] = scale * A * B. a_mn = 0: a is m x k
+ * row-major (K-major); 1: a is k x m row-major (read transposed in place).
+ * b_mn = 1: b is k x n row-major; 0: b is n x k row-major (read transposed). */
+SD_API int sd_gemm_ex(const void* a, int32_t a_mn, const void* b, int32_t b_mn, void* c, int32_t c_dtype,
+                      int32_t m, int32_t n, int32_t k, float scale, void* stream);
+
+/* The paper's comparison baselines (layer.hpp:69-76,105-111,
+ * 148-156): out = in (.) m * scale, bf16 rows x cols (cols % 8 == 0), with m
+ * the reference's per-element counter-hash mask sample_element_mask(seed, p)
+ * (block_mask == NULL, bit-exact) or the expansion of a device BlockMask. */
+SD_API int sd_dropout_apply(const void* in, void* out, int32_t rows, int32_t cols, uint64_t seed, double p,
+                            float scale, const sd_block_mask* block_mask, void* stream);
+
 /* Effective FLOPs (gemm.hpp:217-228): kind 0 = dsd (2*n*m_blk*k_blk*keep),
  * 1 = sdd (2*k*m_blk*n_blk*keep). */
 SD_API uint64_t sd_flops_dense(int64_t m, int64_t n, int64_t k);

@@ -21,6 +21,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <istream>
+#include <ostream>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -269,6 +272,60 @@ inline std::vector<int> kept_blocks_in_row(const BlockMask& mask, int block_row,
         check(sd_stream_synchronize(stream));
     }
     return std::vector<int>(idx.begin(), idx.end());
+}
+
+// ---------------------------------------------------------------- BMSK (block_mask.cpp:137-219)
+// Byte-compatible with the reference's container; read_mask re-compacts the
+// mask on the device so it can drive the GEMMs directly.
+inline void write_mask(const BlockMask& mask, std::ostream& out) {
+    auto put = [&](std::uint64_t v, int n) {
+        for (int i = 0; i < n; ++i) out.put(static_cast<char>((v >> (8 * i)) & 0xff));
+    };
+    out.write("BMSK", 4);
+    out.put(static_cast<char>(0x01));
+    put(static_cast<std::uint32_t>(mask.block_rows()), 4);
+    put(static_cast<std::uint32_t>(mask.block_cols()), 4);
+    put(static_cast<std::uint32_t>(mask.m_blk()), 4);
+    put(static_cast<std::uint32_t>(mask.k_blk()), 4);
+    for (std::uint64_t w : mask.words()) put(w, 8);
+}
+
+inline BlockMask read_mask(std::istream& in, const std::string& name, void* stream = nullptr) {
+    char magic[4];
+    if (!in.read(magic, 4) || std::memcmp(magic, "BMSK", 4) != 0)
+        throw std::runtime_error(name + ": not a BMSK file (bad magic)");
+    const int version = in.get();
+    if (version != 0x01) throw std::runtime_error(name + ": unsupported BMSK version " + std::to_string(version));
+    auto get = [&](int n, const char* what) {
+        unsigned char b[8];
+        if (!in.read(reinterpret_cast<char*>(b), n)) throw std::runtime_error(name + ": truncated BMSK " + what);
+        std::uint64_t v = 0;
+        for (int i = 0; i < n; ++i) v |= std::uint64_t(b[i]) << (8 * i);
+        return v;
+    };
+    const auto br = static_cast<int>(get(4, "header")), bc = static_cast<int>(get(4, "header"));
+    const auto mb = static_cast<int>(get(4, "header")), kb = static_cast<int>(get(4, "header"));
+    if (br <= 0 || bc <= 0 || mb <= 0 || kb <= 0) throw std::runtime_error(name + ": BMSK header has non-positive geometry");
+    std::vector<std::uint64_t> words(static_cast<std::size_t>((static_cast<std::int64_t>(br) * bc + 63) / 64));
+    for (auto& w : words) w = get(8, "payload");
+    try {
+        return mask_from_words(br, bc, mb, kb, words, stream);
+    } catch (const std::invalid_argument& e) {
+        throw std::runtime_error(name + ": " + e.what());
+    }
+}
+
+inline void save_mask(const BlockMask& mask, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+    write_mask(mask, out);
+    if (!out) throw std::runtime_error("write failed: " + path);
+}
+
+inline BlockMask load_mask(const std::string& path, void* stream = nullptr) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    return read_mask(in, path, stream);
 }
 
 // gemm.hpp:31-37 (128-row tile rows; n_blk = 128 on B200)

@@ -60,6 +60,9 @@ class Oracle:
         L.sdo_layer_dx_f64.argtypes = [_p, _p, _p] + [ctypes.c_int] * 5 + [_dbl] + [ctypes.c_int] * 3 + [_p]
         L.sdo_layer_dw_f64.argtypes = [_p, _p, _p] + [ctypes.c_int] * 5 + [_dbl] + [ctypes.c_int] * 3 + [_p]
         L.sdo_dense_gemm_f64.argtypes = [_p, _p] + [ctypes.c_int] * 6 + [_p]
+        L.sdo_element_mask.argtypes = [_u64, _dbl, ctypes.c_int, ctypes.c_int, _p]
+        L.sdo_write_mask.restype = _i64
+        L.sdo_write_mask.argtypes = [_p] + [ctypes.c_int] * 4 + [_p]
 
     def _check(self, rc: int):
         if rc == 0:
@@ -110,6 +113,17 @@ class Oracle:
         out = np.empty((rows, cols), dtype=np.float32)
         self.L.sdo_random_matrix_f32(rows, cols, seed, _np_ptr(out))
         return out
+
+    def element_mask(self, seed, p, rows, cols) -> np.ndarray:
+        out = np.empty((rows, cols), dtype=np.uint8)
+        self.L.sdo_element_mask(seed & (2**64 - 1), p, rows, cols, _np_ptr(out))
+        return out
+
+    def write_mask(self, words, R, C, m_blk, k_blk) -> bytes:
+        buf = np.zeros(21 + 8 * ((R * C + 63) // 64), dtype=np.uint8)
+        n = self.L.sdo_write_mask(_np_ptr(np.ascontiguousarray(words, dtype=np.uint64)), R, C, m_blk, k_blk,
+                                  _np_ptr(buf))
+        return bytes(buf[:n])
 
     def to_bf16_bits(self, a: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(a, dtype=np.float32)
@@ -218,6 +232,39 @@ class Reference:
 
     def counter_hash(self, seed, a, b):
         return int(self.L.sdref_counter_hash(seed, a, b))
+
+    def write_mask(self, words, R, C, m_blk, k_blk) -> bytes:
+        self.L.sdref_write_mask.argtypes = [_p] + [ctypes.c_int] * 4 + [_p, _i64, _p]
+        buf = np.zeros(64 + 8 * ((R * C + 63) // 64), dtype=np.uint8)
+        n = ctypes.c_int64(0)
+        self._check(self.L.sdref_write_mask(_np_ptr(np.ascontiguousarray(words, dtype=np.uint64)), R, C, m_blk,
+                                            k_blk, _np_ptr(buf), len(buf), ctypes.byref(n)))
+        return bytes(buf[: n.value])
+
+    def read_mask(self, data: bytes):
+        self.L.sdref_read_mask.argtypes = [_p, _i64, _p, _p, _i64]
+        arr = np.frombuffer(data, dtype=np.uint8).copy()
+        geom = np.zeros(4, dtype=np.int32)
+        words = np.zeros(max(len(data) // 8 + 1, 1), dtype=np.uint64)
+        self._check(self.L.sdref_read_mask(_np_ptr(arr), len(arr), _np_ptr(geom), _np_ptr(words), len(words)))
+        R, C = int(geom[0]), int(geom[1])
+        return (R, C, int(geom[2]), int(geom[3])), words[: (R * C + 63) // 64].copy()
+
+    def dropout_dense_fwd_bwd(self, x, w, dy, p, seed, step_seed, layer_index, threads=8):
+        L = self.L
+        L.sdref_dropout_dense_fwd_bwd_f64.argtypes = [_p, _p, _p] + [ctypes.c_int] * 3 + [_dbl, _u64, _u64,
+                                                                                            ctypes.c_int, ctypes.c_int,
+                                                                                            _p, _p, _p]
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        dy = np.ascontiguousarray(dy, dtype=np.float64)
+        m, k = x.shape
+        n = w.shape[1]
+        y, dx, dw = np.empty((m, n)), np.empty((m, k)), np.empty((k, n))
+        self._check(L.sdref_dropout_dense_fwd_bwd_f64(_np_ptr(x), _np_ptr(w), _np_ptr(dy), m, n, k, p,
+                                                      seed & (2**64 - 1), step_seed & (2**64 - 1), layer_index,
+                                                      threads, _np_ptr(y), _np_ptr(dx), _np_ptr(dw)))
+        return y, dx, dw
 
     def sample_mask(self, p, m_blk, k_blk, seed, rows, cols):
         cap = max(rows * cols, 64)

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -221,6 +222,48 @@ SDREF_SDD(double, f64)
     }
 SDREF_LAYER(float, f32)
 SDREF_LAYER(double, f64)
+
+// layer.hpp:69-76, 105-111, 148-156: the dropout_dense variant (element mask), double.
+int sdref_dropout_dense_fwd_bwd_f64(const double* x, const double* w, const double* dy, int m, int n, int k,
+                                    double p, uint64_t seed, uint64_t step_seed, int layer_index, int threads,
+                                    double* y, double* dx, double* dw) {
+    return guarded([&] {
+        sparsedrop::LinearLayer<double> layer(sparsedrop::LinearVariant::dropout_dense, mat(w, k, n),
+                                              make_spec(p, 1, 1, seed), sparsedrop::TileConfig{32, 32, 32},
+                                              layer_index);
+        auto fw = sparsedrop::forward(layer, mat(x, m, k), true, step_seed, threads);
+        if (y) out(fw.first, y);
+        auto g = sparsedrop::backward(layer, fw.second, mat(dy, m, n), threads);
+        if (dx) out(g.dx, dx);
+        if (dw) out(g.dw, dw);
+    });
+}
+
+// block_mask.cpp:137-219  write_mask / read_mask (BMSK container)
+int sdref_write_mask(const uint64_t* words, int br, int bc, int m_blk, int k_blk, unsigned char* out,
+                     int64_t cap, int64_t* n_out) {
+    return guarded([&] {
+        std::ostringstream os;
+        sparsedrop::write_mask(mask_of(words, br, bc, m_blk, k_blk), os);
+        const std::string b = os.str();
+        if (static_cast<int64_t>(b.size()) > cap) throw std::runtime_error("sdref_write_mask: buffer too small");
+        std::memcpy(out, b.data(), b.size());
+        *n_out = static_cast<int64_t>(b.size());
+    });
+}
+
+int sdref_read_mask(const unsigned char* bytes, int64_t n, int* geom4, uint64_t* words, int64_t cap) {
+    return guarded([&] {
+        std::istringstream is(std::string(reinterpret_cast<const char*>(bytes), static_cast<std::size_t>(n)));
+        auto m = sparsedrop::read_mask(is, "buffer");
+        geom4[0] = m.block_rows();
+        geom4[1] = m.block_cols();
+        geom4[2] = m.m_blk();
+        geom4[3] = m.k_blk();
+        if (static_cast<int64_t>(m.words().size()) > cap) throw std::runtime_error("sdref_read_mask: buffer too small");
+        std::memcpy(words, m.words().data(), m.words().size() * 8);
+    });
+}
 
 // gemm.hpp:217-228
 uint64_t sdref_flops_dense(int64_t m, int64_t n, int64_t k) { return sparsedrop::flops_dense(m, n, k); }

@@ -167,6 +167,27 @@ int sdo_retile(const uint64_t* words, int R, int C, int m_blk, int k_blk, int sp
     return 0;
 }
 
+/* layer.hpp:69-76 — sample_element_mask: m(i,j) = unit_interval(counter_hash(seed, i, j)) >= p. */
+void sdo_element_mask(uint64_t seed, double p, int rows, int cols, uint8_t* out) {
+    for (int i = 0; i < rows; ++i)
+        for (int j = 0; j < cols; ++j)
+            out[(size_t)i * cols + j] = sdo_unit_interval(sdo_counter_hash(seed, (uint64_t)i, (uint64_t)j)) >= p;
+}
+
+/* block_mask.cpp:137-186 — write_mask: "BMSK", version 0x01, LE u32 block_rows,
+ * block_cols, m_blk, k_blk, then the words as LE u64. Returns the byte count. */
+int64_t sdo_write_mask(const uint64_t* words, int R, int C, int m_blk, int k_blk, uint8_t* out) {
+    int64_t n = 0;
+    out[n++] = 'B'; out[n++] = 'M'; out[n++] = 'S'; out[n++] = 'K'; out[n++] = 0x01;
+    const uint32_t hdr[4] = {(uint32_t)R, (uint32_t)C, (uint32_t)m_blk, (uint32_t)k_blk};
+    for (int h = 0; h < 4; ++h)
+        for (int b = 0; b < 4; ++b) out[n++] = (uint8_t)(hdr[h] >> (8 * b));
+    const int64_t nw = word_count((int64_t)R * C);
+    for (int64_t w = 0; w < nw; ++w)
+        for (int b = 0; b < 8; ++b) out[n++] = (uint8_t)(words[w] >> (8 * b));
+    return n;
+}
+
 /* ---- tests/oracles.hpp ------------------------------------------------- */
 
 /* tests/oracles.hpp:31-41 — random_matrix<float>: |v| in [0.25, 1.25),

@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     sdd_matmul,
     transpose_mask,
 )
+from .bmsk import load_mask, read_mask, save_mask, write_mask  # noqa: F401
 from ._capi import LIB_PATH, NativeLibraryMissing, load as load_library  # noqa: F401
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -80,6 +80,8 @@ PROTOTYPES = {
     "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
     "sd_gelu_forward": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "sd_gelu_backward": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P]),
+    "sd_gemm_ex": (ctypes.c_int, [_P, _I, _P, _I, _P, _I, _I, _I, _I, ctypes.c_float, _P]),
+    "sd_dropout_apply": (ctypes.c_int, [_P, _P, _I, _I, ctypes.c_uint64, ctypes.c_double, ctypes.c_float, _MASKP, _P]),
     "sd_flops_dense": (ctypes.c_uint64, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]),
     "sd_flops_effective": (
         ctypes.c_uint64,

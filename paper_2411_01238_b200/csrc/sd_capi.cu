@@ -551,6 +551,16 @@ int sd_dense_gemm(const void* a, const void* b, void* c, int32_t c_dtype, int32_
     });
 }
 
+int sd_gemm_ex(const void* a, int32_t a_mn, const void* b, int32_t b_mn, void* c, int32_t c_dtype, int32_t m,
+               int32_t n, int32_t k, float scale, void* stream) {
+    return guarded([&] {
+        auto g = prep_dense(a, a_mn != 0, b, b_mn != 0, c, c_dtype, m, n, k);
+        g.args.scale = scale;
+        require_device();
+        launch_gemm(g, as_stream(stream));
+    });
+}
+
 int sd_dense_gemm_nt(const void* a, const void* b_t, void* c, int32_t c_dtype, int32_t m, int32_t n,
                      int32_t k, void* stream) {
     return guarded([&] {

@@ -5,12 +5,21 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "sd_internal.h"
 
 namespace sd {
 namespace {
 
 constexpr int kThreads = 256;
+
+uint64_t mix64_host_eltwise(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
 
 __device__ __forceinline__ float phi_cdf(float x) { return 0.5f * (1.0f + erff(x * 0.70710678118654752f)); }
 
@@ -101,6 +110,87 @@ int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void*
     if (n == 0) return SD_OK;
     gelu_bwd_kernel<<<grid_for(n / 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(h), static_cast<const uint4*>(grad), static_cast<uint4*>(dh), n / 8);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? SD_OK : SD_ERUNTIME;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Dropout-mask application for the paper's comparison baselines (SURVEY §8f2,
+// PAPER.md:161,178, layer.hpp:69-76, 105-111, 148-156):
+//   element mode: m(i,j) = unit_interval(counter_hash(seed, i, j)) >= p
+//                 (sample_element_mask, bit-exact, exact integer threshold)
+//   block mode:   m(i,j) = kept(i / m_blk, j / k_blk) of a device BlockMask
+//   out = in * m * scale   (bf16; the product keeps the reference's signed
+//   zeros: elementwise_mul multiplies, matrix.hpp:80-91)
+namespace sd {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64_dev(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(kThreads) dropout_apply_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                                                 int rows, int cols, uint64_t seed_mix,
+                                                                 uint64_t threshold, float scale,
+                                                                 const uint64_t* __restrict__ words, int m_blk,
+                                                                 int k_blk, int mask_cols) {
+    const int64_t n8 = static_cast<int64_t>(rows) * cols / 8;
+    const int c8 = cols / 8;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int r = static_cast<int>(i / c8);
+        const int c0 = static_cast<int>(i - static_cast<int64_t>(r) * c8) * 8;
+        float x[8];
+        unpack8(ld_nc(in + i), x);
+        if (words) {
+            const int64_t b0 = static_cast<int64_t>(r / m_blk) * mask_cols;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t b = b0 + (c0 + j) / k_blk;
+                const bool keep = (__ldg(words + (b >> 6)) >> (b & 63)) & 1ull;
+                x[j] = x[j] * (keep ? scale : 0.0f);
+            }
+        } else {
+            const uint64_t hr = mix64_dev(seed_mix ^ static_cast<uint64_t>(r));
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint64_t h = mix64_dev(hr ^ static_cast<uint64_t>(c0 + j));
+                x[j] = x[j] * (((h >> 11) >= threshold) ? scale : 0.0f);
+            }
+        }
+        out[i] = pack8(x);
+    }
+}
+
+}  // namespace
+}  // namespace sd
+
+extern "C" {
+
+SD_API int sd_dropout_apply(const void* in, void* out, int32_t rows, int32_t cols, uint64_t seed, double p,
+                            float scale, const sd_block_mask* block_mask, void* stream);
+
+int sd_dropout_apply(const void* in, void* out, int32_t rows, int32_t cols, uint64_t seed, double p, float scale,
+                     const sd_block_mask* block_mask, void* stream) {
+    if (!in || !out || rows <= 0 || cols <= 0 || cols % 8 || reinterpret_cast<uintptr_t>(in) % 16 ||
+        reinterpret_cast<uintptr_t>(out) % 16)
+        return SD_EINVAL;
+    if (block_mask && (block_mask->block_rows * block_mask->m_blk != rows ||
+                       block_mask->block_cols * block_mask->k_blk != cols))
+        return SD_EINVAL;
+    if (!block_mask && !(p >= 0.0 && p < 1.0)) return SD_EINVAL;
+    const uint64_t seed_mix = mix64_host_eltwise(seed);
+    const uint64_t threshold = static_cast<uint64_t>(std::ceil(std::ldexp(p, 53)));
+    const int64_t n8 = static_cast<int64_t>(rows) * cols / 8;
+    dropout_apply_kernel<<<grid_for(n8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(in), static_cast<uint4*>(out), rows, cols, seed_mix, threshold, scale,
+        block_mask ? block_mask->words : nullptr, block_mask ? block_mask->m_blk : 1,
+        block_mask ? block_mask->k_blk : 1, block_mask ? block_mask->block_cols : 1);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? SD_OK : SD_ERUNTIME;
 }

@@ -109,6 +109,26 @@ def main():
     dsd, dsd_cnt = ref.dsd_matmul(a, wm, b, 32, 32, 32, 2.0, dtype=np.float32)
     sdd, sdd_cnt = ref.sdd_matmul(a, b, wm, 32, 32, 32, 1.5, dtype=np.float32)
     np.savez_compressed(OUT / "gemm_ref32.npz", dsd=dsd, sdd=sdd, words=wm, dsd_cnt=dsd_cnt, sdd_cnt=sdd_cnt)
+    # ---- BMSK bytes written by the reference (block_mask.cpp:137-219)
+    bm = []
+    for seed, (p, mb, kb, rows, cols) in enumerate([(0.5, 128, 128, 1024, 1024), (0.4, 2, 3, 12, 12),
+                                                   (0.3, 128, 128, 128 * 13, 128 * 70), (0.9, 1, 1, 5, 7),
+                                                   (0.0, 4, 8, 16, 32)]):
+        w, _ = ref.sample_mask(p, mb, kb, seed, rows, cols)
+        R, C = rows // mb, cols // kb
+        bm.append({"geom": [R, C, mb, kb], "words": [hex(int(x)) for x in w],
+                   "bytes": ref.write_mask(w, R, C, mb, kb).hex()})
+    (OUT / "bmsk.json").write_text(json.dumps(bm, indent=0))
+
+    # ---- dropout_dense variant (element mask) forward/backward, double (layer.hpp:69-76,105-111,148-156)
+    M2, K2, N2 = 256, 256, 128
+    x2 = orc.bf16_bits_to_f64(orc.to_bf16_bits(ref.random_matrix(M2, K2, 1)))
+    w2 = orc.bf16_bits_to_f64(orc.to_bf16_bits(ref.random_matrix(K2, N2, 2)))
+    dy2 = orc.bf16_bits_to_f64(orc.to_bf16_bits(ref.random_matrix(M2, N2, 3)))
+    y2, dx2, dw2 = ref.dropout_dense_fwd_bwd(x2, w2, dy2, 0.3, seed=11, step_seed=2, layer_index=0)
+    np.savez_compressed(OUT / "dropout_dense_256.npz", y=y2.astype(np.float32), dx=dx2.astype(np.float32),
+                        dw=dw2.astype(np.float32), meta=np.array([M2, N2, K2, 11, 2, 0], dtype=np.int64),
+                        p=np.array([0.3]))
     print("golden fixtures written to", OUT)
 
 
