@@ -217,6 +217,12 @@ SD_API uint64_t sd_flops_effective(int64_t n, int64_t k, int32_t m_blk, int32_t 
  * native path ran; see bench.py "gpu_launches"). */
 SD_API uint64_t sd_launch_count(void);
 
+/* Scheduler tuning switches for A/B measurements (default 1):
+ * 1 no tail halving (half-width units for the last wave; measured a net loss),
+ * 2 no split-K, 4 no heaviest-first row order,
+ * 8 backward as two launches instead of one fused launch. */
+SD_API int sd_set_tuning(int32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,7 @@ PROTOTYPES = {
     "sd_last_error": (ctypes.c_char_p, []),
     "sd_device_count": (ctypes.c_int, []),
     "sd_launch_count": (ctypes.c_uint64, []),
+    "sd_set_tuning": (ctypes.c_int, [_I]),
     "sd_device_alloc": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_size_t]),
     "sd_device_free": (ctypes.c_int, [_P]),
     "sd_memcpy": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _I, _P]),

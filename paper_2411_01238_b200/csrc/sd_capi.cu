@@ -234,6 +234,11 @@ const char* sd_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t sd_launch_count(void) { return g_launches.load(); }
 
+int sd_set_tuning(int32_t flags) {
+    set_tuning(flags);
+    return SD_OK;
+}
+
 int sd_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -535,6 +540,11 @@ namespace {
 // with a shared heaviest-first queue — dX's coarse full-reduction units first,
 // dW's finer units fill the tail.
 void fused_backward(const sd::GemmCall& dx, const sd::GemmCall& dw, cudaStream_t s) {
+    if (sd::tuning() & sd::kTuneNoFusedBackward) {
+        sd::launch_gemm(dw, s);
+        sd::launch_gemm(dx, s);
+        return;
+    }
     const sd::GemmCall* calls[2] = {&dx, &dw};
     sd::launch_gemms(calls, 2, s);
 }

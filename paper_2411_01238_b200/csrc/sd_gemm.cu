@@ -53,6 +53,12 @@ __device__ unsigned long long g_sd_trace[1024 * kTraceSlots];
         tr[slot] += clock64() - t0_;                  \
     } while (0)
 #define SD_TADD(slot, v) tr[slot] += (v)
+__device__ unsigned long long g_sd_timeline[256 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #else
 #define SD_TWAIT(slot, expr) expr
 #define SD_TADD(slot, v) ((void)0)
@@ -94,7 +100,7 @@ struct Unit {
     int slot_blk[2];
     int nzero;     // sdd: dropped output blocks in this unit
     int zero_blk[2];
-    int pad[4];    // pad[0]: dsd first list entry of this unit (split-K)
+    int pad[4];    // pad[0]: dsd first list entry (split-K); pad[1]: unit width (256 or 128 in the tail)
 };
 static_assert(sizeof(Unit) == 64, "Unit layout");
 
@@ -105,6 +111,7 @@ struct LaunchArgs {
     GemmArgs p[kMaxProblems];
     int nprob;
     int total_units;
+    int trace_id;  // launch sequence number (SD_TRACE timeline)
     unsigned int* sched;  // {next-unit counter, CTAs-done counter}
 };
 
@@ -116,29 +123,45 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
     Unit t;
     t.prob = prob;
     // split-K (dsd only): the split index is the outermost coordinate
-    const int base_units = a.n_row_tiles * a.n_col_units;
+    const int T = a.tail_rows;
+    const int head_rows = a.n_row_tiles - T;
+    const int head_units = head_rows * a.n_col_units;
+    const int base_units = head_units + T * 2 * a.n_col_units;
     const int split = u / base_units;
     u -= split * base_units;
-    // Grouped rasterization: tile rows (sorted heaviest first) are taken in
-    // groups of kGroupRows; inside a group units go column-unit-major. The
-    // CTAs in flight then share a few operand column/row slabs (L2 reuse), heavy
-    // groups still go first, and for sdd the units carrying MMA work (kept
-    // blocks are packed into the low column units) precede the zero-fill-only
-    // units of their group.
-    const int g = u / (kGroupRows * a.n_col_units);
-    const int rem_u = u - g * kGroupRows * a.n_col_units;
-    const int rows_in_group = min(kGroupRows, a.n_row_tiles - g * kGroupRows);
-    const int cu = rem_u / rows_in_group;
-    const int i = g * kGroupRows + (rem_u - cu * rows_in_group);
+    int i, cu;
+    bool half = false;
+    if (u < head_units) {
+        // Grouped rasterization: tile rows (sorted heaviest first) are taken in
+        // groups of kGroupRows; inside a group units go column-unit-major. The
+        // CTAs in flight then share a few operand column/row slabs (L2 reuse),
+        // heavy groups still go first, and for sdd the units carrying MMA work
+        // (kept blocks are packed into the low column units) precede the
+        // zero-fill-only units of their group.
+        const int g = u / (kGroupRows * a.n_col_units);
+        const int rem_u = u - g * kGroupRows * a.n_col_units;
+        const int rows_in_group = min(kGroupRows, head_rows - g * kGroupRows);
+        cu = rem_u / rows_in_group;
+        i = g * kGroupRows + (rem_u - cu * rows_in_group);
+    } else {
+        // Tail: the lightest rows, handed out last, in half-width units so the
+        // final wave is fine-grained (shorter idle tail across SMs).
+        u -= head_units;
+        cu = u / T;
+        i = head_rows + (u - cu * T);
+        half = true;
+    }
     const int rt = a.row_order ? __ldg(a.row_order + i) : i;
     t.row0 = rt * kBM;
     t.list_row = t.row0 / a.out_row_blk;
     t.nslots = 0;
     t.nzero = 0;
+    const int width = half ? kBN / 2 : kBN;
+    t.pad[1] = width;
     if (!(a.flags & kFlagSDD)) {
-        t.n0 = cu * kBN;
+        t.n0 = cu * width;
         const int rem = a.cols_out - t.n0;
-        t.n_eff = rem < kBN ? rem : kBN;
+        t.n_eff = rem < width ? (rem > 0 ? rem : 0) : width;
         const int cnt = a.list_cnt ? __ldg(a.list_cnt + t.list_row) : a.red / a.red_blk;
         // this split's contiguous share [lo, hi) of the row's kept blocks
         const int lo = static_cast<int>((static_cast<int64_t>(cnt) * split) / a.splits);
@@ -151,7 +174,7 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         // 256-wide units, so every unit but the row's last runs a full N=256 MMA;
         // the same unit index also zero-fills the row's DROPPED blocks (kept at
         // the tail of the list by the mask kernel).
-        const int per_unit = kBN / a.out_col_blk;
+        const int per_unit = width / a.out_col_blk;
         const int cnt = __ldg(a.list_cnt + t.list_row);
         const int ndrop = a.mask_cols - cnt;
         const int32_t* row = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride;
@@ -206,7 +229,8 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
     if (t.n_eff == 0) {
         if (!sdd && !(a.flags & kFlagReduce)) {
             const int rem = a.cols_out - t.n0;
-            zero_rows<OUT_F32>(a, row_first, t.n0, rem < kBN ? rem : kBN, lane);
+            const int w = t.pad[1];
+            if (rem > 0) zero_rows<OUT_F32>(a, row_first, t.n0, rem < w ? rem : w, lane);
         }
         return;
     }
@@ -289,6 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
     const int num_units = L.total_units;
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(L.trace_id & 255) * 4 + 0], gtimer());
+#endif
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 3 * L.nprob; ++i) ptx::prefetch_tmap(&tms.m[i]);
@@ -318,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long tr[16] = {0};
 #ifdef SD_TRACE
     const long long t_start = clock64();
+    if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(L.trace_id & 255) * 4 + 1], gtimer());
 #endif
 
     if (warp == 0) {
@@ -547,6 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(L.trace_id & 255) * 4 + 2], gtimer());
+#endif
     if (threadIdx.x == 0) {
         // last CTA out re-arms the scheduler slot for the next launch
         __threadfence();
@@ -559,6 +590,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace
+
+// Scheduler tuning switches (A/B experiments). Tail halving is off by default:
+// interleaved A/B (tools/ab_tuning.py) showed half-width tail units cost more in
+// operand ingress than they save in idle tail (4096^3: +4% at p=0.5, +11% at p=0.1).
+static int g_tuning = kTuneNoTailHalving;
+int tuning() { return g_tuning; }
+void set_tuning(int t) { g_tuning = t; }
 
 void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
@@ -581,10 +619,11 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     for (int i = 0; i < n; ++i) {
         pa[i] = calls[i]->args;
         pa[i].splits = 1;
+        pa[i].tail_rows = 0;
         const int base = pa[i].n_row_tiles * pa[i].n_col_units;
         const bool sdd = pa[i].flags & kFlagSDD;
         const int red_stages = pa[i].red / kBK;
-        if (!sdd && (pa[i].flags & kFlagF32) && base < 2 * sms && red_stages >= 64) {
+        if (!(g_tuning & kTuneNoSplitK) && !sdd && (pa[i].flags & kFlagF32) && base < 2 * sms && red_stages >= 64) {
             int sp = (2 * sms + base - 1) / base;
             sp = std::min(sp, red_stages / 32);
             if (sp > 1) {
@@ -604,6 +643,19 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
         order[0] = 1;
         order[1] = 0;
     }
+    // tail halving on the problem handed out last, when the launch is only a
+    // few waves deep: its lightest ~2 waves of units become half-width
+    {
+        int total_units = 0;
+        for (int i = 0; i < n; ++i) total_units += gemm_units(pa[i]);
+        GemmArgs& last = pa[order[n - 1]];
+        const bool sdd = last.flags & kFlagSDD;
+        if (!(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units < 12 * sms &&
+            (!sdd || last.out_col_blk == 128)) {
+            const int T = (sms + last.n_col_units - 1) / last.n_col_units;
+            last.tail_rows = std::min(T, last.n_row_tiles);
+        }
+    }
     int total = 0;
     for (int j = 0; j < n; ++j) {
         const int i = order[j];
@@ -611,6 +663,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
         tms.m[3 * j + 1] = calls[i]->tb;
         tms.m[3 * j + 2] = calls[i]->tout;
         L.p[j] = pa[i];
+        if (g_tuning & kTuneNoRowOrder) L.p[j].row_order = nullptr;
         L.p[j].unit_begin = total;
         L.p[j].num_units = gemm_units(L.p[j]);
         total += L.p[j].num_units;
@@ -624,6 +677,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     const int grid = total < cap ? total : cap;
     if (grid <= 0) return;
     L.sched = sched_slot();
+    L.trace_id = static_cast<int>(sd_launch_count());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -641,6 +695,17 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
 }  // namespace sd
 
 #ifdef SD_TRACE
+// timeline: per launch id (mod 256) {first CTA start, first CTA past griddepcontrol.wait, last CTA end}
+extern "C" SD_API int sd_timeline_read(unsigned long long* host) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return SD_ERUNTIME;
+    if (cudaMemcpyFromSymbol(host, g_sd_timeline, sizeof(unsigned long long) * 256 * 4) != cudaSuccess)
+        return SD_ERUNTIME;
+    static unsigned long long init[256 * 4];
+    for (int i = 0; i < 256; ++i) init[4 * i] = init[4 * i + 1] = ~0ull, init[4 * i + 2] = init[4 * i + 3] = 0;
+    cudaMemcpyToSymbol(g_sd_timeline, init, sizeof init);
+    return SD_OK;
+}
+
 extern "C" SD_API int sd_trace_read(unsigned long long* host, int n) {
     if (cudaDeviceSynchronize() != cudaSuccess) return SD_ERUNTIME;
     if (cudaMemcpyFromSymbol(host, g_sd_trace, sizeof(unsigned long long) * n) != cudaSuccess) return SD_ERUNTIME;

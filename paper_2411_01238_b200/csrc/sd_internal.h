@@ -67,11 +67,15 @@ struct GemmArgs {
     void* out;
     unsigned long long* counters;
     int splits;        // dsd split-K factor (>= 1): each unit reduces a contiguous 1/splits of its list
+    int tail_rows;     // the last tail_rows tile rows (lightest, end of the queue) use half-width units
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
 
-inline int gemm_units(const GemmArgs& a) { return a.n_row_tiles * a.n_col_units * (a.splits > 0 ? a.splits : 1); }
+inline int gemm_units(const GemmArgs& a) {
+    const int T = a.tail_rows;
+    return ((a.n_row_tiles - T) * a.n_col_units + T * 2 * a.n_col_units) * (a.splits > 0 ? a.splits : 1);
+}
 
 // A zeroed {counter, done} pair for one persistent-kernel launch (ring of
 // slots per device, re-armed by the last CTA of the launch that used it).
@@ -82,6 +86,11 @@ struct GemmCall {
     CUtensorMap ta, tb, tout;
     GemmArgs args;
 };
+
+// Scheduler tuning switches (bitmask; 0 = everything on), for A/B runs.
+enum TuneFlags : int { kTuneNoTailHalving = 1, kTuneNoSplitK = 2, kTuneNoRowOrder = 4, kTuneNoFusedBackward = 8 };
+int tuning();
+void set_tuning(int t);
 
 // Launch 1 or 2 independent GEMM problems as ONE persistent kernel sharing a
 // single heaviest-first work queue (problem 0's units are handed out first).

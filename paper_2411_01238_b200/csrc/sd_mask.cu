@@ -36,7 +36,17 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+#ifdef SD_TRACE
+__device__ unsigned long long g_sd_timeline[256 * 4];  // this TU's copy (mask launches)
+__device__ __forceinline__ unsigned long long gtimer_m() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 struct PlanArgs {
+    int trace_id;
     sd_block_mask m;
     int from_words;
     uint64_t seed_mix;   // mix64(seed): counter_hash = mix64(mix64(seed_mix ^ r) ^ c)
@@ -128,6 +138,9 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     // the consumer GEMM may start its prologue now; its griddepcontrol.wait
     // still orders all of its reads after this grid completes
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(a.trace_id & 255) * 4 + 0], gtimer_m());
+#endif
     // our own inputs (mask words in compact mode) come from earlier work
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -224,6 +237,9 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     order_by_count(a.m.row_cnt, R, C, a.m.row_order, dyn_smem, warp_tot);
     order_by_count(a.m.col_cnt, C, R, a.m.col_order, dyn_smem, warp_tot);
     if (threadIdx.x == 0) *a.m.ticket = 0u;  // re-arm for the next launch on this workspace
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
+#endif
 }
 
 __device__ __forceinline__ bool in_bit(const uint64_t* w, int64_t b) { return (w[b >> 6] >> (b & 63)) & 1ull; }
@@ -264,6 +280,7 @@ __global__ void mask_retile_kernel(const uint64_t* in, int R, int C, int sm, int
 void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix, uint64_t threshold,
                       cudaStream_t s) {
     PlanArgs a;
+    a.trace_id = static_cast<int>(sd_launch_count());
     a.m = m;
     a.from_words = from_words ? 1 : 0;
     a.seed_mix = seed_mix;
@@ -320,3 +337,15 @@ void launch_mask_retile(const sd_block_mask& in, int split_m, int split_k, sd_bl
 }
 
 }  // namespace sd
+
+#ifdef SD_TRACE
+extern "C" SD_API int sd_mask_timeline_read(unsigned long long* host) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return SD_ERUNTIME;
+    if (cudaMemcpyFromSymbol(host, sd::g_sd_timeline, sizeof(unsigned long long) * 256 * 4) != cudaSuccess)
+        return SD_ERUNTIME;
+    static unsigned long long init[256 * 4];
+    for (int i = 0; i < 256; ++i) init[4 * i] = init[4 * i + 1] = ~0ull, init[4 * i + 2] = init[4 * i + 3] = 0;
+    cudaMemcpyToSymbol(sd::g_sd_timeline, init, sizeof init);
+    return SD_OK;
+}
+#endif
