@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (headline loop only)")
     ap.add_argument("--preroll", type=float, default=0.3, help="seconds of sustained load before each timing")
+    ap.add_argument("--rotate", type=int, default=3,
+                    help="input sets cycled step to step (their combined size exceeds L2, so steps run "
+                         "back-to-back without an L2 flush)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (CI check of the data-parallel path)")
     return ap.parse_args()
@@ -63,7 +66,8 @@ def workload_config(size, p, world):
         "M_per_gpu": size, "N": size, "K": size, "M_global": size * world,
         "m_blk": 128, "k_blk": 128, "p": p, "seed": 0,
         "dtypes": {"x/w/dy/y/dx": "bf16", "dw": "fp32", "accumulate": "fp32"},
-        "l2": "flushed between timed steps (512 MiB device write outside the timed events)",
+        "l2": "inputs larger than L2: steps rotate over several input sets whose combined footprint exceeds "
+              "the 126 MB L2 (see 'timing')",
         "parallelism": f"dp{world} row-sharded (shard-local masks, dW all-reduce)" if world > 1 else "single GPU",
     }
 
@@ -267,12 +271,16 @@ def main():
         sign = torch.where(torch.rand(r, c, generator=gen, device=dev) < 0.5, -1.0, 1.0)
         return ((0.25 + u) * sign).to(torch.bfloat16)
 
-    x = synth(M, K)
     gen_w = torch.Generator(device=dev)
     gen_w.manual_seed(99)  # W replicated: same on every rank
-    w = ((0.25 + torch.rand(K, N, generator=gen_w, device=dev)) *
-         torch.where(torch.rand(K, N, generator=gen_w, device=dev) < 0.5, -1.0, 1.0)).to(torch.bfloat16)
-    dy = synth(M, N)
+    n_sets = max(1, args.rotate)
+    sets = []
+    for _ in range(n_sets):
+        w_ = ((0.25 + torch.rand(K, N, generator=gen_w, device=dev)) *
+              torch.where(torch.rand(K, N, generator=gen_w, device=dev) < 0.5, -1.0, 1.0)).to(torch.bfloat16)
+        sets.append((synth(M, K), w_, synth(M, N)))
+    x, w, dy = sets[0]
+    set_bytes = (M * K + K * N + M * N) * 2
     flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
     row_off = rank * (M // 128)
@@ -280,12 +288,15 @@ def main():
     def flush():
         flush_buf.fill_(float(len(str(flush_buf.numel()))))
 
-    def time_steps(step, steps, warmup, preroll_s=None):
+    def time_steps(step, steps, warmup, preroll_s=None, rotate=None):
         preroll_s = args.preroll if preroll_s is None else preroll_s
-        """Sum of per-step CUDA-event durations on the launching stream (L2 flushed
-        before every step, outside the events); max over ranks. A short sustained
-        pre-roll of the same step first, so every configuration is timed in the
-        same (power-capped) steady state rather than a cold burst."""
+        rotate = (n_sets > 1) if rotate is None else rotate
+        """Device time per step (CUDA events on the launching stream, max over
+        ranks). rotate: steps run back-to-back, each on the next of `n_sets`
+        input sets whose combined footprint exceeds L2; else: L2 flushed before
+        every step outside the per-step events. A short sustained pre-roll of
+        the same step first, so every configuration is timed in the same
+        (power-capped) steady state rather than a cold burst."""
         if preroll_s > 0:
             # estimate the step time, then run the same number of pre-roll steps
             # on every rank (each step may contain a collective)
@@ -301,37 +312,56 @@ def main():
                 if j % 64 == 63:
                     torch.cuda.synchronize()
         for i in range(warmup):
-            flush()
+            if not rotate:
+                flush()
             step(i)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         l0 = sd.launch_count()
-        for i in range(steps):
-            flush()
-            evs[i][0].record()
-            step(warmup + i)
-            evs[i][1].record()
-        torch.cuda.synchronize()
+        if rotate:
+            # back-to-back steps over rotating input sets (combined > L2): one
+            # event pair around exactly `steps` steps
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for i in range(steps):
+                step(warmup + i)
+            b.record()
+            torch.cuda.synchronize()
+            total_ms = a.elapsed_time(b)
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(steps)]
+            for i in range(steps):
+                flush()
+                evs[i][0].record()
+                step(warmup + i)
+                evs[i][1].record()
+            torch.cuda.synchronize()
+            total_ms = sum(a_.elapsed_time(b_) for a_, b_ in evs)
         barrier()
         torch.cuda.synchronize()
         launch_box[0] = sd.launch_count() - l0
-        total_ms = sum(a.elapsed_time(b) for a, b in evs)
         return max_over_ranks(total_ms) / steps
 
     plans = {}
     launch_box = [0]
 
-    def plan_for(p):
-        if p not in plans:
-            plans[p] = sd.LayerPlan(x, w, dy, p, row_block_offset=row_off)
-        return plans[p]
+    def plan_for(p, j=0):
+        if (p, j) not in plans:
+            xs, ws, dys = sets[j]
+            plans[(p, j)] = sd.LayerPlan(xs, ws, dys, p, row_block_offset=row_off)
+        return plans[(p, j)]
+
+    def drop_plans(p):
+        for j in range(n_sets):
+            plans.pop((p, j), None)
 
     def sparse_step_fn(p):
-        plan = plan_for(p)
+        pls = [plan_for(p, j) for j in range(n_sets)]
 
         def step(i):
+            plan = pls[i % n_sets]
             plan.forward(seed=sd.effective_seed(0, i, 0))
             if world > 1:
                 plan.backward_dw()
@@ -346,9 +376,10 @@ def main():
         return step
 
     def dense_step_fn():
-        plan = plan_for(args.p)
+        pls = [plan_for(args.p, j) for j in range(n_sets)]
 
         def step(i):
+            plan = pls[i % n_sets]
             plan.dense_forward()
             if world > 1:
                 plan.dense_backward()  # dw then dx on the compute stream
@@ -362,9 +393,10 @@ def main():
         return step
 
     def torch_step(i):
-        y = x @ w
-        dw = x.t() @ dy
-        dx = dy @ w.t()
+        xs, ws, dys = sets[i % n_sets]
+        y = xs @ ws
+        dw = xs.t() @ dys
+        dx = dys @ ws.t()
         return y, dw, dx
 
     flops_dense_step = 3 * 2 * M * N * K  # per GPU
@@ -376,7 +408,8 @@ def main():
         # samples see the clocks the timed steps run at
         ms = time_steps(head_step, args.steps, args.warmup,
                         preroll_s=0.2 if args.profile else max(args.preroll, 1.5 if args.preroll > 0 else 0.0))
-    gpu_launches = launch_box[0]  # our kernels enqueued inside the timed region (4 per step)
+    gpu_launches = launch_box[0]  # our kernels enqueued inside the timed region (3 per step)
+    ms_isolated = time_steps(head_step, args.steps, args.warmup, rotate=False) if not args.profile else None
     plan = plan_for(args.p)
     keep = plan.mask.keep_count() / plan.mask.total_blocks()
     value = world * flops_dense_step / (ms * 1e-3) / 1e12
@@ -391,33 +424,50 @@ def main():
     ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup)
     ms_torch = time_steps(torch_step, args.steps, args.warmup)
 
-    # ---- per-kernel durations at the headline p (roofline)
-    def kernel_ms(fn, steps):
-        for _ in range(3):
-            flush(); fn()
-        torch.cuda.synchronize()
-        tot = 0.0
-        for _ in range(steps):
-            flush()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(); fn(); b.record()
-            torch.cuda.synchronize()
-            tot += a.elapsed_time(b)
-        return tot / steps
+    # ---- per-kernel durations at the headline p (roofline): each kernel run
+    # back-to-back over the rotating input sets, one event pair around them
+    lib = sd.load_library()
+    import ctypes as _ct
 
+    def rot_ms(fns, steps):
+        for j in range(3 * n_sets):
+            fns[j % n_sets]()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for i in range(steps):
+            fns[i % n_sets]()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    pls = [plan_for(args.p, j) for j in range(n_sets)]
+    st_ = lambda: _ct.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+
+    def fwd_only(pl):
+        return lambda: sd.api.check(lib.sd_linear_forward(pl.x.data_ptr(), pl.mask.cptr(), pl.w.data_ptr(), pl.scale,
+                                                          pl.y.data_ptr(), 1, M, N, K, st_()))
+
+    for pl in pls:
+        pl.forward(seed=7)
     keep_blocks = plan.mask.keep_count()
     exec_flops = 2 * N * 128 * 128 * keep_blocks  # flops_effective (gemm.hpp:222-228), per GEMM
+    ksteps = max(args.steps, 10)
     kms = {
-        "mask_gen+compact": kernel_ms(lambda: sd.sample_mask(sd.DropoutSpec(args.p, 128, 128, 7), M, K,
-                                                            row_block_offset=row_off, out=plan.mask), args.steps),
-        "dsd_fwd": kernel_ms(lambda: plan.forward(seed=7), args.steps),
-        "dsd_dw": kernel_ms(plan.backward_dw, args.steps),
-        "sdd_dx": kernel_ms(plan.backward_dx, args.steps),
+        "mask_gen+compact": rot_ms([lambda pl=pl: sd.sample_mask(sd.DropoutSpec(args.p, 128, 128, 7), M, K,
+                                                                 row_block_offset=row_off, out=pl.mask)
+                                    for pl in pls], ksteps),
+        "dsd_fwd": rot_ms([fwd_only(pl) for pl in pls], ksteps),
+        "bwd_fused(dsd_dw+sdd_dx)": rot_ms([pl.backward for pl in pls], ksteps),
+        "dsd_dw(standalone)": rot_ms([pl.backward_dw for pl in pls], ksteps),
+        "sdd_dx(standalone)": rot_ms([pl.backward_dx for pl in pls], ksteps),
     }
-    kms["dsd_fwd"] = max(kms["dsd_fwd"] - kms["mask_gen+compact"], 1e-6)  # plan.forward = mask + fwd
-    gemm_k = {k: v for k, v in kms.items() if k != "mask_gen+compact"}
-    dom = max(gemm_k, key=gemm_k.get)
-    achieved = exec_flops / (gemm_k[dom] * 1e-3) / 1e12
+    kflops = {"dsd_fwd": exec_flops, "bwd_fused(dsd_dw+sdd_dx)": 2 * exec_flops, "dsd_dw(standalone)": exec_flops,
+              "sdd_dx(standalone)": exec_flops}
+    # the dominant kernel of the step as it runs: the longest of forward / fused backward
+    dom = max(("dsd_fwd", "bwd_fused(dsd_dw+sdd_dx)"), key=kms.get)
+    achieved = kflops[dom] / (kms[dom] * 1e-3) / 1e12
+    exec_flops_dom = kflops[dom]
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -434,12 +484,17 @@ def main():
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": dom,
-        "algorithmic_per_launch": {"flops": exec_flops, "note": "keep_count*2*N*128*128 (flops_effective)"},
+        "algorithmic_per_launch": {"flops": exec_flops_dom,
+                                   "note": "keep_count*2*N*128*128 per GEMM (flops_effective, gemm.hpp:222-228); "
+                                           "the fused backward launch carries dW + dX"},
+        "per_kernel_tflops": {k: kflops[k] / (kms[k] * 1e-3) / 1e12 for k in kflops},
         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)" if peaks
         else "fallback 1590 (B200_PROFILING.md)",
         "peak_sustained": float(peaks.get("bf16_tflops_sustained", 1400.0)),
         "frac_of_sustained": achieved / float(peaks.get("bf16_tflops_sustained", 1400.0)),
         "kernel_ms": kms,
+        "kernel_timing": "each kernel back-to-back over the rotating input sets (mask_gen is host-launch-bound "
+                         "here; ncu: ~5-7 us)",
     }
 
     # ---- sweep
@@ -457,7 +512,7 @@ def main():
                 "time_vs_dense_over_keep": (msp / ms_dense) / max(kp, 1e-9),
             })
             if p != args.p:
-                plans.pop(p, None)
+                drop_plans(p)
 
     # ---- T8: the north-star 8192^3 target (sparse p=0.1/0.5 vs our dense), single GPU only
     t8 = None
@@ -541,6 +596,10 @@ def main():
             "config": workload_config(S, args.p, world),
             "keep_fraction": keep, "executed_tflops": value * keep,
             "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
+            "isolated_ms_per_step": ms_isolated,
+            "timing": (f"{n_sets} rotating input sets ({n_sets * set_bytes / 2**20:.0f} MiB > L2), steps back-to-back, "
+                       "one CUDA-event pair around the K timed steps; isolated_ms_per_step: one step at a time "
+                       "with a 512 MiB L2 flush before each, per-step events (includes launch latency)"),
             "torch_cublas_dense_ms_per_step": ms_torch,
             "gpu_launches": gpu_launches,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

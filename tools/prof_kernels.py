@@ -19,7 +19,9 @@ dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
 y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 dx = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
 dw = torch.empty(K, N, device="cuda", dtype=torch.float32)
-m = sd.sample_mask(sd.DropoutSpec(P, 128, 128, 0), M, K)
+plan = sd.LayerPlan(x, w, dy, P)
+plan.forward(0)
+m = plan.mask
 s = sd.dropout_scale(P)
 
 
@@ -35,6 +37,7 @@ fns = {
     "dense_nt": lambda: lib.sd_dense_gemm_nt(dy.data_ptr(), w.data_ptr(), dx.data_ptr(), 1, M, K, N, st()),
     "dense_tn": lambda: lib.sd_dense_gemm_tn(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, K, N, M, st()),
     "mask": lambda: sd.sample_mask(sd.DropoutSpec(P, 128, 128, 1), M, K, out=m),
+    "bwd": lambda: plan.backward(),
 }
 for _ in range(2):
     for k in which:

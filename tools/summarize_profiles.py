@@ -22,7 +22,8 @@ prof = ROOT / "profiles"
 prof.mkdir(exist_ok=True)
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-ROLE = {"<0, 1, 0, 0>": "dsd_fwd", "<1, 1, 0, 1>": "dsd_dw", "<0, 0, 1, 0>": "sdd_dx", "mask_plan": "mask_gen+compact"}
+# capture order of tools/capture_profiles.sh (all GEMMs share one kernel name)
+ROLES_IN_ORDER = ["mask_gen+compact", "dsd_fwd", "bwd_fused(dsd_dw+sdd_dx)"]
 
 rep = g / f"{tag}_full.ncu-rep"
 if rep.exists():
@@ -30,8 +31,8 @@ if rep.exists():
     with redirect_stdout(buf):
         res = ncu_summary.full(str(rep))
     out, traffic = [], {}
-    for e in res:
-        role = next((v for k, v in ROLE.items() if k in e["kernel"]), e["kernel"][:60])
+    for idx, e in enumerate(res):
+        role = ROLES_IN_ORDER[idx] if idx < len(ROLES_IN_ORDER) else e["kernel"][:60]
         e["role"] = role
         rd = e.get("dram_read", 0) * UNIT.get(e.get("dram_read_unit", "byte"), 1)
         wr = e.get("dram_write", 0) * UNIT.get(e.get("dram_write_unit", "byte"), 1)
