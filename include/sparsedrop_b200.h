@@ -220,7 +220,9 @@ SD_API uint64_t sd_launch_count(void);
 /* Scheduler tuning switches for A/B measurements (default 1):
  * 1 no tail halving (half-width units for the last wave; measured a net loss),
  * 2 no split-K, 4 no heaviest-first row order,
- * 8 backward as two launches instead of one fused launch. */
+ * 8 backward as two launches instead of one fused launch,
+ * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA
+ *    (cta_group::2) kernel. */
 SD_API int sd_set_tuning(int32_t flags);
 
 #ifdef __cplusplus

@@ -606,6 +606,21 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
                    "cudaFuncSetAttribute(max dynamic smem)");
         configured = true;
     }
+    // dense problems go to the 2-CTA kernel (half the per-SM operand traffic
+    // per MAC: tools/gemm2_check.py, +10-25% over this kernel at 4096-8192)
+    if (!(g_tuning & kTuneNoGemm2)) {
+        bool dense = true;
+        for (int i = 0; i < n; ++i) {
+            const GemmArgs& a = calls[i]->args;
+            dense = dense && a.list_cnt == nullptr && a.counters == nullptr && gemm2_supported(a) &&
+                    (a.rows_out / 256) * (a.cols_out / 256) >= num_sms() / 2;
+        }
+        if (dense) {
+            for (int i = 0; i < n; ++i)
+                launch_gemm2(calls[i]->ta, calls[i]->tb, calls[i]->tout, calls[i]->args, nullptr, nullptr, 0, s);
+            return;
+        }
+    }
     TensorMaps tms;
     LaunchArgs L;
     std::memset(&L, 0, sizeof L);

@@ -1,0 +1,373 @@
+// sd_gemm2.cu — the 2-CTA (cta_group::2) tcgen05 GEMM for dense-mask work.
+//
+// A CTA pair (cluster of 2, one TPC) computes a 256 x 256 output tile with
+// one M=256 / N=256 tcgen05.mma per K=16 step issued by the leader CTA:
+//   CTA r holds A rows [128 r, 128 r + 128) and B columns [128 r, 128 r + 128)
+//   of the tile, so each SM ingests 32 KB per 64-deep stage instead of the
+//   1-CTA kernel's 48 KB for the same MACs per SM — the per-SM TMA ingress
+//   (~80 B/clk, profiles/r01_load_path_diag.txt) stops being the bound.
+// Pair protocol:
+//   full barrier    leader only; both CTAs' TMAs complete_tx on it (peer bit
+//                   cleared), the peer adds a remote arrive
+//   empty barrier   each CTA; the leader's commit multicasts to both
+//   TMEM full       each CTA; the leader's commit multicasts to both
+//   TMEM empty      leader only; all 8 epilogue warps of the pair arrive
+// Union mode (dsd with a list per 128-row block): the pair's two row blocks
+// walk the UNION of their kept lists; a CTA whose own row dropped a block
+// zero-fills its A stage instead of loading it, so the dropped block still
+// contributes exact zeros (no wrong results, only redundant MMA work). Used
+// when the mask keeps most blocks (low p), where halving ingress beats the
+// extra MMA work.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sd_internal.h"
+#include "sd_ptx.cuh"
+
+namespace sd {
+namespace {
+
+constexpr int kStages2 = 6;
+constexpr int kHalfBytes = 128 * kBK * 2;  // 16 KB: one CTA's half of A or B per stage
+constexpr int kEpiWarps = 4;
+constexpr int kEpiBufBytes = 32 * 128;
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+constexpr int kTile = 256;  // pair tile: 256 x 256
+
+constexpr int kOffA = 0;
+constexpr int kOffB = kOffA + kStages2 * kHalfBytes;
+constexpr int kOffEpi = kOffB + kStages2 * kHalfBytes;
+constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+constexpr int kNumBars = 2 * kStages2 + 4;
+constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
+constexpr int kSmemBytes2 = kOffTmemSlot + 16 + 1024;
+static_assert(kSmemBytes2 <= 232448, "shared memory budget");
+
+// 2-SM TMA load: completes tx on the LEADER's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_2sm(const void* tmap, uint64_t* bar, void* dst, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(ptx::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void commit2_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                     "r"(ptx::smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+
+struct Pair2Args {
+    GemmArgs g;         // rows_out, cols_out, red, flags (kFlagAMN/BMN/F32), scale, out, list*, red_blk, out_row_blk
+    int n_pair_rows;    // rows_out / 256
+    int n_col_tiles;    // cols_out / 256
+    // union mode: for each 256-row pair, the merged kept list with an owner mask
+    const int32_t* pair_cnt;   // [n_pair_rows]
+    const int32_t* pair_idx;   // [n_pair_rows][list_stride]: (block << 2) | owner_mask(bit0 = row 2i, bit1 = 2i+1)
+    int pair_stride;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
+    sd_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmOut, const Pair2Args P) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+    const uint32_t sbase = ptx::smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    uint64_t* full_bar = bars;               // leader only
+    uint64_t* empty_bar = bars + kStages2;   // each CTA
+    uint64_t* tfull_bar = bars + 2 * kStages2;
+    uint64_t* tempty_bar = bars + 2 * kStages2 + 2;  // leader only
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+
+    const GemmArgs& a = P.g;
+    const uint32_t warp = threadIdx.x / 32;
+    const uint32_t lane = ptx::lane_id();
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const bool a_mn = a.flags & kFlagAMN, b_mn = a.flags & kFlagBMN, f32 = a.flags & kFlagF32;
+    const bool unioned = P.pair_cnt != nullptr;
+    const int num_units = P.n_pair_rows * P.n_col_tiles;
+    const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmOut);
+        for (int i = 0; i < kStages2; ++i) {
+            ptx::mbar_init(full_bar + i, 2);  // leader's expect_tx arrive + peer's remote arrive
+            ptx::mbar_init(empty_bar + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(tfull_bar + i, 1);
+            ptx::mbar_init(tempty_bar + i, 2 * kEpiWarps);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+
+    // static schedule over pair units, heaviest pair rows first (pair rows are
+    // ordered by the host/mask planner), column-tile-major within groups of 8
+    auto decode = [&](int u, int& prow, int& ct) {
+        constexpr int G = 8;
+        const int g = u / (G * P.n_col_tiles);
+        const int rem = u - g * G * P.n_col_tiles;
+        const int rows_in_group = min(G, P.n_pair_rows - g * G);
+        ct = rem / rows_in_group;
+        prow = g * G + (rem - ct * rows_in_group);
+    };
+    auto unit_stages = [&](int prow) -> int {
+        if (unioned) return __ldg(P.pair_cnt + prow) * (a.red_blk / kBK);
+        return a.red / kBK;
+    };
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = cluster_id; u < num_units; u += n_clusters) {
+                int prow, ct;
+                decode(u, prow, ct);
+                const int nst = unit_stages(prow);
+                const int row0 = prow * kTile + 128 * static_cast<int>(rank);  // this CTA's A rows
+                const int col0 = ct * kTile + 128 * static_cast<int>(rank);    // this CTA's B columns
+                const int spb = a.red_blk / kBK;
+                const int32_t* lst = unioned ? P.pair_idx + static_cast<int64_t>(prow) * P.pair_stride : nullptr;
+                int entry = 0;
+                for (int s = 0; s < nst; ++s) {
+                    int r0;
+                    bool own = true;
+                    if (unioned) {
+                        if (s % spb == 0) entry = __ldg(lst + s / spb);
+                        r0 = (entry >> 2) * a.red_blk + (s % spb) * kBK;
+                        own = (entry >> rank) & 1;
+                    } else {
+                        r0 = s * kBK;
+                    }
+                    ptx::mbar_wait(empty_bar + stage, phase ^ 1);
+                    uint8_t* sA = smem + kOffA + stage * kHalfBytes;
+                    uint8_t* sB = smem + kOffB + stage * kHalfBytes;
+                    const uint32_t my_bytes = (own ? kHalfBytes : 0) + kHalfBytes;
+                    if (!own) {
+                        // own row dropped this block: exact zeros into the A half
+                        // (generic-proxy stores made visible to the tensor core)
+                        uint4* z = reinterpret_cast<uint4*>(sA);
+                        for (int i = 0; i < kHalfBytes / 16; ++i) z[i] = make_uint4(0, 0, 0, 0);
+                        ptx::fence_proxy_async_smem();
+                    }
+                    if (leader) {
+                        // expect both CTAs' bytes: peer's own-ness comes from the same entry
+                        const bool peer_own = unioned ? ((entry >> 1) & 1) : true;
+                        const uint32_t peer_bytes = (peer_own ? kHalfBytes : 0) + kHalfBytes;
+                        ptx::mbar_arrive_expect_tx(full_bar + stage, my_bytes + peer_bytes);
+                    } else {
+                        ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(full_bar + stage), 0));
+                    }
+                    if (own) {
+                        if (!a_mn) {
+                            tma_load_2sm(&tmA, full_bar + stage, sA, r0, row0);
+                        } else {
+                            tma_load_2sm(&tmA, full_bar + stage, sA, row0, r0);
+                            tma_load_2sm(&tmA, full_bar + stage, sA + 8192, row0 + 64, r0);
+                        }
+                    }
+                    if (!b_mn) {
+                        tma_load_2sm(&tmB, full_bar + stage, sB, r0, col0);
+                    } else {
+                        tma_load_2sm(&tmB, full_bar + stage, sB, col0, r0);
+                        tma_load_2sm(&tmB, full_bar + stage, sB + 8192, col0 + 64, r0);
+                    }
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader only) =====================
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t acc_iter = 0;
+            const uint32_t idesc = ptx::make_idesc_bf16(256, 256, a_mn, b_mn);
+            const uint32_t a_step = a_mn ? 2048u : 32u, b_step = b_mn ? 2048u : 32u;
+            const uint32_t a_lbo = a_mn ? 8192u : 0u, b_lbo = b_mn ? 8192u : 0u;
+            for (int u = cluster_id; u < num_units; u += n_clusters) {
+                int prow, ct;
+                decode(u, prow, ct);
+                const int nst = unit_stages(prow);
+                if (nst == 0) continue;
+                const uint32_t acc = acc_iter & 1;
+                const uint32_t acc_phase = (acc_iter >> 1) & 1;
+                ++acc_iter;
+                ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kTile;
+                for (int s = 0; s < nst; ++s) {
+                    ptx::mbar_wait(full_bar + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = sbase + kOffA + stage * kHalfBytes;
+                    const uint32_t b_addr = sbase + kOffB + stage * kHalfBytes;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                        const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
+                        mma2_bf16(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    }
+                    commit2_mc(empty_bar + stage, 0x3);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                commit2_mc(tfull_bar + acc, 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (both CTAs, own 128 rows) =====================
+        const uint32_t q = warp & 3;
+        uint8_t* ebuf = smem + kOffEpi + q * 2 * kEpiBufBytes;
+        const uint32_t ebuf_addr = sbase + kOffEpi + q * 2 * kEpiBufBytes;
+        uint32_t bi = 0, acc_iter = 0;
+        const int chunk = f32 ? 32 : 64;
+        const int esz = f32 ? 4 : 2;
+        for (int u = cluster_id; u < num_units; u += n_clusters) {
+            int prow, ct;
+            decode(u, prow, ct);
+            const int row_first = prow * kTile + 128 * static_cast<int>(rank) + 32 * q;
+            if (unit_stages(prow) == 0) {
+                // both rows of the pair fully dropped: exact zeros
+                char* base = static_cast<char*>(a.out);
+                const int cpr = kTile * esz / 16;
+                for (int idx = lane; idx < 32 * cpr; idx += 32) {
+                    const int r = idx / cpr, c = idx - r * cpr;
+                    ptx::st_global_v4_zero(base + (static_cast<int64_t>(row_first + r) * a.cols_out + ct * kTile) * esz +
+                                           c * 16);
+                }
+                continue;
+            }
+            const uint32_t acc = acc_iter & 1;
+            const uint32_t acc_phase = (acc_iter >> 1) & 1;
+            ++acc_iter;
+            ptx::mbar_wait(tfull_bar + acc, acc_phase);
+            ptx::tc_fence_after();
+            const int nchunks = kTile / chunk;
+            for (int c = 0; c < nchunks; ++c) {
+                const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kTile + c * chunk;
+                uint32_t v[64];
+                ptx::tmem_ld_32x32b_x32(taddr, v);
+                if (!f32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
+                ptx::tmem_ld_wait();
+                if (c == nchunks - 1) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(tempty_bar + acc), 0));
+                }
+                if (lane == 0) ptx::bulk_wait_group_read<1>();
+                __syncwarp();
+                const uint32_t row_addr = ebuf_addr + bi * kEpiBufBytes + lane * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t w0, w1, w2, w3;
+                    if (f32) {
+                        w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * a.scale);
+                        w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * a.scale);
+                        w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * a.scale);
+                        w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * a.scale);
+                    } else {
+                        const float* f = reinterpret_cast<const float*>(v) + 8 * j;
+                        w0 = ptx::pack_bf16x2(f[0] * a.scale, f[1] * a.scale);
+                        w1 = ptx::pack_bf16x2(f[2] * a.scale, f[3] * a.scale);
+                        w2 = ptx::pack_bf16x2(f[4] * a.scale, f[5] * a.scale);
+                        w3 = ptx::pack_bf16x2(f[6] * a.scale, f[7] * a.scale);
+                    }
+                    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), w0, w1, w2, w3);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, ct * kTile + c * chunk, row_first);
+                    ptx::bulk_commit_group();
+                }
+                bi ^= 1;
+            }
+        }
+        if (lane == 0) ptx::bulk_wait_group<0>();
+        __syncwarp();
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+}
+
+}  // namespace
+
+bool gemm2_supported(const GemmArgs& a) {
+    return !(a.flags & (kFlagSDD | kFlagReduce)) && a.rows_out % 256 == 0 && a.cols_out % 256 == 0 &&
+           a.red % kBK == 0;
+}
+
+void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
+                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2),
+                   "cudaFuncSetAttribute(gemm2 smem)");
+        configured = true;
+    }
+    Pair2Args P;
+    std::memset(&P, 0, sizeof P);
+    P.g = g;
+    P.n_pair_rows = g.rows_out / 256;
+    P.n_col_tiles = g.cols_out / 256;
+    P.pair_cnt = pair_cnt;
+    P.pair_idx = pair_idx;
+    P.pair_stride = pair_stride;
+    const int units = P.n_pair_rows * P.n_col_tiles;
+    int clusters = std::min(units, num_sms() / 2);
+    if (clusters <= 0) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes2;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel, ta, tb, tout, P), "sd_gemm2_kernel launch");
+    note_launch();
+}
+
+}  // namespace sd

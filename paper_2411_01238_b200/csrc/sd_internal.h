@@ -88,7 +88,13 @@ struct GemmCall {
 };
 
 // Scheduler tuning switches (bitmask; 0 = everything on), for A/B runs.
-enum TuneFlags : int { kTuneNoTailHalving = 1, kTuneNoSplitK = 2, kTuneNoRowOrder = 4, kTuneNoFusedBackward = 8 };
+enum TuneFlags : int {
+    kTuneNoTailHalving = 1,
+    kTuneNoSplitK = 2,
+    kTuneNoRowOrder = 4,
+    kTuneNoFusedBackward = 8,
+    kTuneNoGemm2 = 16,  // dense problems on the 1-CTA kernel instead of the 2-CTA one
+};
 int tuning();
 void set_tuning(int t);
 
@@ -99,6 +105,13 @@ inline void launch_gemm(const GemmCall& c, cudaStream_t s) {
     const GemmCall* p = &c;
     launch_gemms(&p, 1, s);
 }
+
+// 2-CTA (cta_group::2) kernel for dense problems (no mask list): 256 x 256
+// pair tiles, static schedule. Used by launch_gemms when every problem of the
+// launch is dense and has at least one wave of pair tiles.
+bool gemm2_supported(const GemmArgs& a);
+void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
+                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s);
 
 // 2D row-major tensor map: `inner` contiguous elements, `outer` rows, 128B swizzle.
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,

@@ -161,8 +161,10 @@ def test_mask_validation(sd):
 
 # --------------------------------------------------------------------------- dense
 
+# (2560, 2048, 512) and (2304, 2304, 320) have >= 74 256x256 pair tiles and run
+# on the 2-CTA (cta_group::2) kernel; the others on the 1-CTA kernel
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 256), (1024, 1024, 1024), (384, 640, 192),
-                                   (512, 384, 4096)])
+                                   (512, 384, 4096), (2560, 2048, 512), (2304, 2304, 320)])
 @pytest.mark.parametrize("layout", ["nn", "nt", "tn"])
 def test_dense_gemm(sd, oracle, M, N, K, layout):
     a = _dev(oracle, M, K, 1)
@@ -183,6 +185,37 @@ def test_dense_gemm(sd, oracle, M, N, K, layout):
             sd.api.check(lib.sd_dense_gemm_tn(at.data_ptr(), b.data_ptr(), c.data_ptr(), code, M, N, K, st))
         torch.cuda.synchronize()
         (check_f32 if dt == torch.float32 else check_bf16)(_np(c), ref, _abs_prod(an, bn))
+
+
+@pytest.mark.parametrize("layout", ["nn", "nt", "tn"])
+def test_dense_2cta_equals_1cta_bitwise(sd, oracle, layout):
+    """The 2-CTA kernel accumulates every output element over the same K16
+    steps in the same order as the 1-CTA kernel: results are bit-identical."""
+    M, N, K = 4096, 2048, 768
+    a = _dev(oracle, M, K, 1)
+    b = _dev(oracle, K, N, 2)
+    lib = sd.load_library()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    outs = {}
+    try:
+        for tune in (1 | 16, 1):
+            lib.sd_set_tuning(tune)
+            for dt, code in [(torch.float32, 0), (torch.bfloat16, 1)]:
+                c = torch.empty(M, N, dtype=dt, device="cuda")
+                if layout == "nn":
+                    sd.dense_gemm(a, b, out=c)
+                elif layout == "nt":
+                    bt = b.t().contiguous()
+                    sd.api.check(lib.sd_dense_gemm_nt(a.data_ptr(), bt.data_ptr(), c.data_ptr(), code, M, N, K, st))
+                else:
+                    at = a.t().contiguous()
+                    sd.api.check(lib.sd_dense_gemm_tn(at.data_ptr(), b.data_ptr(), c.data_ptr(), code, M, N, K, st))
+                outs[(tune, code)] = c
+        torch.cuda.synchronize()
+    finally:
+        lib.sd_set_tuning(1)
+    for code in (0, 1):
+        assert torch.equal(outs[(1 | 16, code)], outs[(1, code)])
 
 
 # --------------------------------------------------------------------------- dsd forward
