@@ -145,10 +145,14 @@ CUtensorMap out_map(void* c, int dt, int rows, int cols) {
     return make_tmap_2d(c, f32, cols, rows, f32 ? 32 : 64, 32);
 }
 
-// bf16 operand maps. K-major (reduction contiguous): box 64 x 128 rows.
-// MN-major (output dimension contiguous): box 64 x 64 reduction rows.
+// bf16 operand maps, 16 KB boxes. K-major (reduction contiguous): box 64 x
+// 128 rows. MN-major (output dimension contiguous): a 3D box of two 64-wide
+// atoms x 64 reduction rows. Per-SM TMA throughput is bound by boxes, not
+// bytes (tools/l2_bench.cu: five boxes per 48 KB stage cap an SM at ~117 GB/s,
+// two reach ~240 GB/s), so an operand tile is loaded in as few boxes as the
+// 128B swizzle allows.
 CUtensorMap kmajor_map(const void* p, int red, int rows) { return make_tmap_2d(p, false, red, rows, 64, 128); }
-CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_2d(p, false, mn, red, 64, 64); }
+CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_mn_atoms(p, mn, red); }
 
 }  // namespace
 
@@ -192,8 +196,8 @@ unsigned int* sched_slot() {
     return slots[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
 }
 
-CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                         uint32_t box_outer) {
+static CUtensorMap encode_tmap(const void* base, bool f32, cuuint32_t rank, const cuuint64_t* dims,
+                               const cuuint64_t* strides, const cuuint32_t* box) {
     std::call_once(g_encode_once, [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -208,18 +212,35 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
         fail(SD_ERUNTIME, "cuTensorMapEncodeTiled unavailable (driver too old?)");
     }
     CUtensorMap map;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = g_encode(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                                const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::string shape;
+        for (cuuint32_t i = 0; i < rank; ++i) shape += (i ? "x" : "") + std::to_string(dims[rank - 1 - i]);
+        fail(SD_ERUNTIME, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ") for a " +
+                              shape + " tensor");
+    }
+    return map;
+}
+
+CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                         uint32_t box_outer) {
     const cuuint64_t dims[2] = {inner, outer};
     const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
     const cuuint32_t box[2] = {box_inner, box_outer};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = g_encode(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                                2, const_cast<void*>(base), dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-        fail(SD_ERUNTIME, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
-                              ") for a " + std::to_string(outer) + "x" + std::to_string(inner) + " tensor");
-    return map;
+    return encode_tmap(base, f32, 2, dims, strides, box);
+}
+
+CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red) {
+    // view [red][mn] (mn contiguous) as (64 mn_in, red, mn / 64 atoms): one box
+    // = two 64-wide SW128 atoms of 64 reduction rows, atom-major in smem
+    const cuuint64_t dims[3] = {64, red, mn / 64};
+    const cuuint64_t strides[2] = {mn * 2, 128};
+    const cuuint32_t box[3] = {64, 64, 2};
+    return encode_tmap(base, false, 3, dims, strides, box);
 }
 
 }  // namespace sd

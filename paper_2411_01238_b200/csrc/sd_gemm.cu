@@ -23,13 +23,15 @@
 //   warp 0      TMA producer (one lane): 4-stage smem ring, mbarrier full/empty
 //   warp 1      MMA issuer (one lane): tcgen05.mma -> TMEM, tcgen05.commit
 //   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warp 3      scheduler (one lane): claims + decodes units
 //   warps 4..7  epilogue: tcgen05.ld -> scale -> bf16/fp32 -> swizzled smem
 //               -> TMA store; all-dropped tiles written as +0.0 directly.
 // Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
-// Scheduling is dynamic: the producer steals units from a global atomic counter
-// (units ordered heaviest first, grouped for L2 reuse; problem 0 before problem
-// 1), decodes them (list lookups) and hands the decoded unit to the MMA and
-// epilogue roles through a shared-memory ring; zero-work units skip TMEM.
+// Scheduling is dynamic: the scheduler warp steals units from a global atomic
+// counter (units ordered heaviest first, grouped for L2 reuse; problem 0 before
+// problem 1) when the producer nears the end of its current unit, decodes them
+// (list lookups) and hands the decoded unit to the producer, MMA and epilogue
+// roles through a shared-memory ring; zero-work units skip TMEM.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -71,6 +73,9 @@ namespace {
 #define SD_STAGES 4
 #endif
 constexpr int kStages = SD_STAGES;
+#ifndef SD_CLAIM_LEAD
+#define SD_CLAIM_LEAD 6  // stages before a unit's last load at which the next unit is claimed
+#endif
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 constexpr int kBBytes = kBN * kBK * 2;  // 32 KB per stage
 constexpr int kEpiWarps = 4;
@@ -85,7 +90,7 @@ constexpr int kOffEpi = kOffB + kStages * kBBytes;
 constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
 constexpr int kGroupRows = 16;  // tile rows per rasterization group
 constexpr int kSchedDepth = 4;  // decoded-unit ring between the producer and the consumers
-constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth;
+constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth + 1;
 constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
 constexpr int kOffSched = kOffTmemSlot + 16;
 
@@ -104,7 +109,9 @@ struct Unit {
 };
 static_assert(sizeof(Unit) == 64, "Unit layout");
 
-constexpr int kSmemBytes = kOffSched + static_cast<int>(sizeof(Unit)) * kSchedDepth + 1024;  // + align slack
+constexpr int kListCap = 64;  // kept-block list entries staged per ring slot (longer lists: __ldg)
+constexpr int kOffList = kOffSched + static_cast<int>(sizeof(Unit)) * kSchedDepth;
+constexpr int kSmemBytes = kOffList + kListCap * 4 * kSchedDepth + 1024;  // + align slack
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 struct LaunchArgs {
@@ -307,8 +314,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = bars + 2 * kStages + 2;
     uint64_t* sfull_bar = bars + 2 * kStages + 4;
     uint64_t* sempty_bar = sfull_bar + kSchedDepth;
+    uint64_t* claim_bar = sempty_bar + kSchedDepth;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
     Unit* sched_unit = reinterpret_cast<Unit*>(smem + kOffSched);
+    int32_t* sched_list = reinterpret_cast<int32_t*>(smem + kOffList);  // [kSchedDepth][kListCap]
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
@@ -329,8 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < kSchedDepth; ++i) {
             ptx::mbar_init(sfull_bar + i, 1);
-            ptx::mbar_init(sempty_bar + i, 1 + kEpiWarps);
+            ptx::mbar_init(sempty_bar + i, 2 + kEpiWarps);  // producer, MMA, epilogue warps
         }
+        ptx::mbar_init(claim_bar, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -345,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long tr[16] = {0};
 #ifdef SD_TRACE
     const long long t_start = clock64();
+    const unsigned long long g_start = gtimer();
     if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(L.trace_id & 255) * 4 + 1], gtimer());
 #endif
 
@@ -356,33 +367,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int sslot = 0;
             uint32_t sphase = 0;
-            // Dynamic persistent scheduling: first unit = blockIdx.x, then work
-            // stealing through a global atomic counter (units are ordered
-            // heaviest first, so this is greedy longest-processing-time).
-            int u = blockIdx.x;
-            int nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
-            Unit t;
-            if (u < num_units) t = decode_global(L, u); else t.prob = -1;
+            // Units come from the scheduler warp through the ring; kClaimLead
+            // stages before this unit's loads are all issued, the scheduler is
+            // told to claim the next one (see warp 3).
+            constexpr int kClaimLead = SD_CLAIM_LEAD;
             while (true) {
-                SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
-                sched_unit[sslot] = t;
-                ptx::mbar_arrive(sfull_bar + sslot);
+                SD_TWAIT(1, ptx::mbar_wait(sfull_bar + sslot, sphase));
+                const Unit cur = sched_unit[sslot];
+                const int cur_slot = sslot;
                 if (++sslot == kSchedDepth) {
                     sslot = 0;
                     sphase ^= 1;
                 }
-                if (t.prob < 0) break;
-                // decode the next unit now: its global loads (and the atomic
-                // for the one after) overlap this unit's TMA stream
-                const Unit cur = t;
-                u = nxt;
-                if (u < num_units) {
-                    nxt = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
-                    t = decode_global(L, u);
-                } else {
-                    t.prob = -1;
+                if (cur.prob < 0) {
+                    ptx::mbar_arrive(sempty_bar + cur_slot);
+                    break;
                 }
-                if (cur.n_eff == 0) continue;
+                const int nst = cur.n_eff == 0 ? 0 : cur.nstages;
+                const int claim_at = nst > kClaimLead ? nst - kClaimLead : 0;
+                if (nst == 0) {
+                    ptx::mbar_arrive(sempty_bar + cur_slot);
+                    ptx::mbar_arrive(claim_bar);
+                    continue;
+                }
                 const GemmArgs& a = L.p[cur.prob];
                 const CUtensorMap* tmA = &tms.m[3 * cur.prob];
                 const CUtensorMap* tmB = &tms.m[3 * cur.prob + 1];
@@ -395,15 +402,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t* lst =
                     (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
                                          : nullptr;
-                // kept-block index prefetched one block ahead (off the TMA issue path)
-                int kb_next = lst ? __ldg(lst) : 0;
+                // kept-block indices: staged in smem by the scheduler (lists up to
+                // kListCap), else read from global one block ahead
+                const int32_t* slist = sched_list + cur_slot * kListCap;
+                const bool staged = cur.nstages / spb <= kListCap;
+                int kb_next = lst ? (staged ? slist[0] : __ldg(lst)) : 0;
                 int kb = 0;
                 for (int s = 0, li = 0, sub = 0; s < cur.nstages; ++s) {
+                    if (s == claim_at) ptx::mbar_arrive(claim_bar);
                     int r0;
                     if (!sdd) {
                         if (sub == 0) {
                             kb = lst ? kb_next : li0 + li;
-                            if (lst && li + 1 < cur.nstages / spb) kb_next = __ldg(lst + li + 1);
+                            if (lst && li + 1 < cur.nstages / spb) kb_next = staged ? slist[li + 1] : __ldg(lst + li + 1);
                         }
                         r0 = kb * a.red_blk + sub * kBK;
                         if (++sub == spb) {
@@ -430,16 +441,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!a_mn) {
                         ptx::tma_load_2d(tmA, fb, sA, r0, cur.row0, pol);
                     } else {
-                        ptx::tma_load_2d(tmA, fb, sA, cur.row0, r0, pol);
-                        ptx::tma_load_2d(tmA, fb, sA + 8192, cur.row0 + 64, r0, pol);
+                        ptx::tma_load_3d(tmA, fb, sA, 0, r0, cur.row0 / 64, pol);
                     }
                     if (!sdd) {
                         if (!b_mn) {
                             for (int j = 0; j < cur.n_eff / 128; ++j)
                                 ptx::tma_load_2d(tmB, fb, sB + j * 16384, r0, cur.n0 + 128 * j, pol);
                         } else {
-                            for (int j = 0; j < cur.n_eff / 64; ++j)
-                                ptx::tma_load_2d(tmB, fb, sB + j * 8192, cur.n0 + 64 * j, r0, pol);
+                            for (int j = 0; j < cur.n_eff / 128; ++j)
+                                ptx::tma_load_3d(tmB, fb, sB + j * 16384, 0, r0, (cur.n0 + 128 * j) / 64, pol);
                         }
                     } else {
                         for (int sl = 0; sl < cur.nslots; ++sl) {
@@ -449,9 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 for (int j = 0; j < per; ++j)
                                     ptx::tma_load_2d(tmB, fb, sB + (sl * per + j) * 16384, r0, col0 + 128 * j, pol);
                             } else {
-                                const int per = a.out_col_blk / 64;
+                                const int per = a.out_col_blk / 128;
                                 for (int j = 0; j < per; ++j)
-                                    ptx::tma_load_2d(tmB, fb, sB + (sl * per + j) * 8192, col0 + 64 * j, r0, pol);
+                                    ptx::tma_load_3d(tmB, fb, sB + (sl * per + j) * 16384, 0, r0, (col0 + 128 * j) / 64,
+                                                     pol);
                             }
                         }
                     }
@@ -460,7 +471,61 @@ __global__ void __launch_bounds__(kThreads, 1)
                         phase ^= 1;
                     }
                 }
+                ptx::mbar_arrive(sempty_bar + cur_slot);  // done with the slot's staged list
             }
+        }
+    } else if (warp == 3) {
+        // ===================== scheduler =====================
+        // Dynamic persistent scheduling: first unit = blockIdx.x, then work
+        // stealing through a global atomic counter (units are ordered heaviest
+        // first, so this is greedy longest-processing-time). The next unit is
+        // claimed only when the producer nears the end of its current one:
+        // late enough that a CTA never sits on a claimed unit while others idle
+        // at the tail (claiming two units ahead cost 15-40% tail imbalance),
+        // early enough that the atomic and the decode's dependent loads (here,
+        // off the TMA issue path) finish before the producer needs the unit.
+        // The whole warp stages the unit's kept-block list (dsd) into the slot's
+        // smem list, so the producer never waits on a list load between TMAs.
+        int sslot = 0;
+        uint32_t sphase = 0;
+        uint32_t cphase = 0;
+        int u = blockIdx.x;
+        while (true) {
+            Unit t;
+            if (lane == 0) {
+                if (u < num_units) t = decode_global(L, u); else t.prob = -1;
+            }
+            // list source of this unit (dsd with a list): entries [li0, li0 + nblk)
+            const int32_t* src = nullptr;
+            int nblk = 0;
+            if (lane == 0 && t.prob >= 0 && t.n_eff > 0) {
+                const GemmArgs& a = L.p[t.prob];
+                if (!(a.flags & kFlagSDD) && a.list_idx) {
+                    src = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride + t.pad[0];
+                    nblk = t.nstages / (a.red_blk / kBK);
+                }
+            }
+            src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), 0));
+            nblk = __shfl_sync(0xffffffffu, nblk, 0);
+            if (lane == 0) SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
+            __syncwarp();
+            for (int i = lane; i < nblk && i < kListCap; i += 32) sched_list[sslot * kListCap + i] = __ldg(src + i);
+            __syncwarp();
+            const int prob = __shfl_sync(0xffffffffu, t.prob, 0);
+            if (lane == 0) {
+                sched_unit[sslot] = t;
+                ptx::mbar_arrive(sfull_bar + sslot);  // release: the list stores above are visible
+            }
+            if (++sslot == kSchedDepth) {
+                sslot = 0;
+                sphase ^= 1;
+            }
+            if (prob < 0) break;
+            if (lane == 0) {
+                ptx::mbar_wait(claim_bar, cphase);
+                u = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
+            }
+            cphase ^= 1;
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
@@ -563,9 +628,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (warp == 1 && lane == 0) {
             atomicAdd(out + 2, tr[2]); atomicAdd(out + 3, tr[3]); atomicAdd(out + 4, tr[4]);
             atomicAdd(out + 7, t_role_end - t_start); atomicAdd(out + 8, tr[8]);
+            // globaltimer of this CTA's run (ns) and its start relative to the launch's first CTA
+            atomicAdd(out + 12, gtimer() - g_start);
+            atomicAdd(out + 13, g_start);
         } else if (warp == 4 && lane == 0) {
             atomicAdd(out + 5, tr[5]); atomicAdd(out + 6, tr[6]); atomicAdd(out + 10, t_role_end - t_start);
             atomicAdd(out + 11, tr[11]);
+            atomicAdd(out + 14, gtimer() - g_start);  // epilogue role end (ns after start)
         }
     }
 #else
@@ -653,8 +722,11 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     }
     // one shared queue, heaviest units first: the problem with the larger
     // per-unit cost is handed out first
+    // (dsd cost is an upper bound — only kept blocks are reduced — while sdd
+    // units always run the full reduction, so ties go to the sdd problem)
     int order[kMaxProblems] = {0, 1};
-    if (n == 2 && cost[1] > cost[0]) {
+    const bool sdd0 = pa[0].flags & kFlagSDD, sdd1 = n == 2 && (pa[1].flags & kFlagSDD);
+    if (n == 2 && (cost[1] > cost[0] || (cost[1] == cost[0] && sdd1 && !sdd0))) {
         order[0] = 1;
         order[1] = 0;
     }

@@ -48,6 +48,14 @@ constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
 constexpr int kSmemBytes2 = kOffTmemSlot + 16 + 1024;
 static_assert(kSmemBytes2 <= 232448, "shared memory budget");
 
+__device__ __forceinline__ void tma_load_2sm_3d(const void* tmap, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(ptx::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
 // 2-SM TMA load: completes tx on the LEADER's barrier (peer bit cleared)
 __device__ __forceinline__ void tma_load_2sm(const void* tmap, uint64_t* bar, void* dst, int32_t c0, int32_t c1) {
     asm volatile(
@@ -194,15 +202,13 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                         if (!a_mn) {
                             tma_load_2sm(&tmA, full_bar + stage, sA, r0, row0);
                         } else {
-                            tma_load_2sm(&tmA, full_bar + stage, sA, row0, r0);
-                            tma_load_2sm(&tmA, full_bar + stage, sA + 8192, row0 + 64, r0);
+                            tma_load_2sm_3d(&tmA, full_bar + stage, sA, 0, r0, row0 / 64);
                         }
                     }
                     if (!b_mn) {
                         tma_load_2sm(&tmB, full_bar + stage, sB, r0, col0);
                     } else {
-                        tma_load_2sm(&tmB, full_bar + stage, sB, col0, r0);
-                        tma_load_2sm(&tmB, full_bar + stage, sB + 8192, col0 + 64, r0);
+                        tma_load_2sm_3d(&tmB, full_bar + stage, sB, 0, r0, col0 / 64);
                     }
                     if (++stage == kStages2) {
                         stage = 0;

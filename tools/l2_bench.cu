@@ -156,11 +156,124 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Ring-shape variant: `nst` stages of `nbox` 16 KB boxes, distinct streams.
+__global__ void __launch_bounds__(128, 1) l2_ring(const __grid_constant__ CUtensorMap tm, int nst, int nbox,
+                                                 long long total_bytes, unsigned long long* t_out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = nbox * 16384;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) mbar_init(full + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned long long t0 = gtimer();
+    if (threadIdx.x == 0) {
+        const int stages_total = static_cast<int>(total_bytes / stage_bytes);
+        int tile = (blockIdx.x * 97 * 3) % kTiles;
+        for (int s = 0; s < stages_total; ++s) {
+            const int st = s % nst;
+            if (s >= nst) mbar_wait(full + st, ((s / nst) - 1) & 1);
+            mbar_expect_tx(full + st, stage_bytes);
+            for (int j = 0; j < nbox; ++j) {
+                const int t = (tile + j) % kTiles;
+                tma_load(&tm, full + st, smem + st * stage_bytes + j * 16384, (t % kTilesK) * 64, (t / kTilesK) * 128);
+            }
+            tile = (tile + nbox) % kTiles;
+        }
+        for (int s = stages_total; s < stages_total + nst; ++s) mbar_wait(full + s % nst, ((s / nst) - 1) & 1);
+        t_out[2 * blockIdx.x] = t0;
+        t_out[2 * blockIdx.x + 1] = gtimer();
+    }
+}
+
+// GEMM-shaped stages: one 16 KB A box {64,128} + nb 8 KB B boxes {64,64}.
+__global__ void __launch_bounds__(128, 1) l2_gemm_ring(const __grid_constant__ CUtensorMap tmA,
+                                                      const __grid_constant__ CUtensorMap tmB, int nst, int nb,
+                                                      long long total_bytes, unsigned long long* t_out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = 16384 + nb * 8192;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) mbar_init(full + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned long long t0 = gtimer();
+    if (threadIdx.x == 0) {
+        const int stages_total = static_cast<int>(total_bytes / stage_bytes);
+        int ta = (blockIdx.x * 97) % kTiles, tb = (blockIdx.x * 193) % (2 * kTiles);
+        for (int s = 0; s < stages_total; ++s) {
+            const int st = s % nst;
+            if (s >= nst) mbar_wait(full + st, ((s / nst) - 1) & 1);
+            mbar_expect_tx(full + st, stage_bytes);
+            uint8_t* base = smem + st * stage_bytes;
+            tma_load(&tmA, full + st, base, (ta % kTilesK) * 64, (ta / kTilesK) * 128);
+            for (int j = 0; j < nb; ++j) {
+                const int t = (tb + j) % (2 * kTiles);
+                tma_load(&tmB, full + st, base + 16384 + j * 8192, (t % kTilesK) * 64, (t / kTilesK) * 64);
+            }
+            ta = (ta + 1) % kTiles;
+            tb = (tb + nb) % (2 * kTiles);
+        }
+        for (int s = stages_total; s < stages_total + nst; ++s) mbar_wait(full + s % nst, ((s / nst) - 1) & 1);
+        t_out[2 * blockIdx.x] = t0;
+        t_out[2 * blockIdx.x + 1] = gtimer();
+    }
+}
+
+__device__ __forceinline__ void tma_load3(const CUtensorMap* tm, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// GEMM-shaped stages with ONE 3D box for B: {64 n, 64 k, nb n-atoms} = nb * 8 KB
+// laid out atom-major (the MN-major SW128 operand layout), plus the A box.
+__global__ void __launch_bounds__(128, 1) l2_gemm3d_ring(const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmB3, int nst, int nb,
+                                                        long long total_bytes, unsigned long long* t_out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = 16384 + nb * 8192;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) mbar_init(full + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned long long t0 = gtimer();
+    if (threadIdx.x == 0) {
+        const int stages_total = static_cast<int>(total_bytes / stage_bytes);
+        int ta = (blockIdx.x * 97) % kTiles;
+        int kb = (blockIdx.x * 13) % (kRows / 64), nt = (blockIdx.x * 7) % (kCols / (64 * nb));
+        for (int s = 0; s < stages_total; ++s) {
+            const int st = s % nst;
+            if (s >= nst) mbar_wait(full + st, ((s / nst) - 1) & 1);
+            mbar_expect_tx(full + st, stage_bytes);
+            uint8_t* base = smem + st * stage_bytes;
+            tma_load(&tmA, full + st, base, (ta % kTilesK) * 64, (ta / kTilesK) * 128);
+            tma_load3(&tmB3, full + st, base + 16384, 0, kb * 64, nt * nb);
+            ta = (ta + 1) % kTiles;
+            kb = (kb + 1) % (kRows / 64);
+            if (kb == 0) nt = (nt + 1) % (kCols / (64 * nb));
+        }
+        for (int s = stages_total; s < stages_total + nst; ++s) mbar_wait(full + s % nst, ((s / nst) - 1) & 1);
+        t_out[2 * blockIdx.x] = t0;
+        t_out[2 * blockIdx.x + 1] = gtimer();
+    }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int main(int argc, char** argv) {
+    const bool quick = argc > 1;
+    setvbuf(stdout, nullptr, _IONBF, 0);
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     void* buf = nullptr;
@@ -178,6 +291,7 @@ int main() {
         std::printf("encode failed\n");
         return 1;
     }
+    if (quick) return 0;
     CUtensorMap tm64;
     cuuint32_t box64[2] = {64, 64};
     if (reinterpret_cast<EncodeFn>(fn)(&tm64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box64, es,
@@ -194,10 +308,12 @@ int main() {
     std::vector<unsigned long long> t(2 * 1024);
     const int stages_total = 400;
     for (int ctas : {sms, sms / 2, 32}) {
+        if (quick && ctas != sms) continue;
         for (int group : {1, 2, 4, 8, 16, 148}) {
+            if (quick && group > 2) continue;
             if (group > ctas) continue;
             double best = 0;
-            for (int rep = 0; rep < 3; ++rep) {
+            for (int rep = 0; rep < (quick ? 1 : 3); ++rep) {
                 l2_stream<<<ctas, 128, smem>>>(tm, group, 0, stages_total, t_dev);
                 CK(cudaDeviceSynchronize());
                 CK(cudaMemcpy(t.data(), t_dev, 2 * ctas * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -230,6 +346,93 @@ int main() {
         }
         std::printf("ctas %3d cluster-2 multicast halves: delivered %7.1f GB/s total, %6.1f GB/s per SM\n", ctas, best,
                     best / ctas);
+    }
+    CK(cudaFuncSetAttribute(l2_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int shapes[][2] = {{4, 3}, {3, 3}, {2, 3}, {2, 5}, {2, 4}, {3, 4}, {5, 2}, {6, 2}, {4, 2}, {8, 1}, {12, 1}};
+    for (auto& sh : shapes) {
+        const int smem_r = sh[0] * sh[1] * 16384 + 1024 + 256;
+        if (smem_r > 227 * 1024) continue;
+        for (int ctas : {sms, 37}) {
+            double best = 0;
+            for (int rep = 0; rep < 3; ++rep) {
+                l2_ring<<<ctas, 128, smem_r>>>(tm, sh[0], sh[1], 400ll * 48 * 1024, t_dev);
+                CK(cudaDeviceSynchronize());
+                CK(cudaMemcpy(t.data(), t_dev, 2 * ctas * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+                unsigned long long lo = ~0ull, hi = 0;
+                for (int c = 0; c < ctas; ++c) {
+                    lo = t[2 * c] < lo ? t[2 * c] : lo;
+                    hi = t[2 * c + 1] > hi ? t[2 * c + 1] : hi;
+                }
+                const double gbs = double(ctas) * 400.0 * 48 * 1024 / double(hi - lo);
+                best = gbs > best ? gbs : best;
+            }
+            std::printf("ring %d x %3d KB (%3d KB in flight) ctas %3d: %7.1f GB/s total, %6.1f GB/s per SM\n", sh[0],
+                        sh[1] * 16, sh[0] * sh[1] * 16, ctas, best, best / ctas);
+        }
+    }
+    CK(cudaFuncSetAttribute(l2_gemm_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int gshapes[][2] = {{4, 4}, {3, 4}, {2, 8}, {3, 6}};
+    for (auto& sh : gshapes) {
+        const int sb = 16384 + sh[1] * 8192;
+        const int smem_r = sh[0] * sb + 1024 + 256;
+        if (smem_r > 227 * 1024) continue;
+        for (int ctas : {sms, 37}) {
+            double best = 0;
+            for (int rep = 0; rep < 3; ++rep) {
+                l2_gemm_ring<<<ctas, 128, smem_r>>>(tm, tm64, sh[0], sh[1], 400ll * 48 * 1024, t_dev);
+                CK(cudaDeviceSynchronize());
+                CK(cudaMemcpy(t.data(), t_dev, 2 * ctas * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+                unsigned long long lo = ~0ull, hi = 0;
+                for (int c = 0; c < ctas; ++c) {
+                    lo = t[2 * c] < lo ? t[2 * c] : lo;
+                    hi = t[2 * c + 1] > hi ? t[2 * c + 1] : hi;
+                }
+                const double gbs = double(ctas) * 400.0 * 48 * 1024 / double(hi - lo);
+                best = gbs > best ? gbs : best;
+            }
+            std::printf("gemm ring %d x (A16 + %d x B8 = %3d KB) ctas %3d: %7.1f GB/s total, %6.1f GB/s per SM\n", sh[0],
+                        sh[1], sb / 1024, ctas, best, best / ctas);
+        }
+    }
+    {
+        // 3D view of the row-major [kRows][kCols] matrix: (n_in 64, k rows, n_out atoms)
+        CUtensorMap tm3;
+        cuuint64_t d3[3] = {64, kRows, kCols / 64}, s3[2] = {kCols * 2, 128};
+        cuuint32_t es3[3] = {1, 1, 1};
+        CK(cudaFuncSetAttribute(l2_gemm3d_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        for (int nb : {4, 8}) {
+            cuuint32_t b3[3] = {64, 64, (cuuint32_t)nb};
+            CUresult r = reinterpret_cast<EncodeFn>(fn)(&tm3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, d3, s3, b3, es3,
+                                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != 0) {
+                std::printf("3d encode failed (%d) for nb=%d\n", (int)r, nb);
+                continue;
+            }
+            for (int nst : {2, 3, 4}) {
+                const int sb = 16384 + nb * 8192;
+                const int smem_r = nst * sb + 1024 + 256;
+                if (smem_r > 227 * 1024) continue;
+                for (int ctas : {sms, 37}) {
+                    double best = 0;
+                    for (int rep = 0; rep < 3; ++rep) {
+                        l2_gemm3d_ring<<<ctas, 128, smem_r>>>(tm, tm3, nst, nb, 400ll * 48 * 1024, t_dev);
+                        CK(cudaDeviceSynchronize());
+                        CK(cudaMemcpy(t.data(), t_dev, 2 * ctas * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+                        unsigned long long lo = ~0ull, hi = 0;
+                        for (int c = 0; c < ctas; ++c) {
+                            lo = t[2 * c] < lo ? t[2 * c] : lo;
+                            hi = t[2 * c + 1] > hi ? t[2 * c + 1] : hi;
+                        }
+                        const double gbs = double(ctas) * 400.0 * 48 * 1024 / double(hi - lo);
+                        best = gbs > best ? gbs : best;
+                    }
+                    std::printf("gemm3d ring %d x (A16 + B3d %d KB = %3d KB, 2 boxes) ctas %3d: %7.1f GB/s total, %6.1f GB/s per SM\n",
+                                nst, nb * 8, sb / 1024, ctas, best, best / ctas);
+                }
+            }
+        }
     }
     // how far apart in time may two readers of the same tiles be and still share?
     for (int lag : {0, 1, 2, 4, 8, 16, 32, 64, 128}) {

@@ -39,11 +39,17 @@ fns = {
     "mask": lambda: sd.sample_mask(sd.DropoutSpec(P, 128, 128, 1), M, K, out=m),
     "bwd": lambda: plan.backward(),
 }
+def run(k):
+    r = fns[k]()
+    if isinstance(r, int) and r != 0:
+        raise RuntimeError(f"{k}: {sd.api.last_error() if hasattr(sd.api, 'last_error') else r}")
+
+
 for _ in range(2):
     for k in which:
-        fns[k]()
+        run(k)
 torch.cuda.synchronize()
 for k in which:
-    fns[k]()
+    run(k)
 torch.cuda.synchronize()
 print("done", S, P, which)

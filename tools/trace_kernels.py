@@ -67,6 +67,15 @@ for name, fn in fns.items():
     r = {n: t[active, i].mean() for i, n in enumerate(names)}
     frac = lambda k: r[k] / r["mma_run"]  # noqa: E731
     mma_busy = 1 - frac("mma_wait_full") - frac("mma_wait_tmem") - frac("mma_wait_sched")
+    if not active.any():
+        print(f"{name:10s} {ms * 1e3:7.1f}us  (not on the traced 1-CTA kernel)")
+        continue
+    g_run = t[active, 12]; g_st = t[active, 13]; e_run = t[active, 14]
+    ghz = (run[active] / np.maximum(g_run, 1)).mean()
+    g0 = g_st.min()
+    print(f"{name:10s} clock64 {ghz:.2f} GHz | CTA start spread {(g_st.max() - g0) / 1e3:.1f} us | "
+          f"MMA run ns mean {g_run.mean() / 1e3:.1f} max {g_run.max() / 1e3:.1f} us | epi end max "
+          f"{(e_run + g_st - g0).max() / 1e3:.1f} us after first start")
     print(f"{name:10s} {ms * 1e3:7.1f}us  mma_run={r['mma_run'] / 1e3:6.1f}kcyc (max {run.max() / 1e3:6.1f}, "
           f"min {run[active].min() / 1e3:6.1f})  wait_full={frac('mma_wait_full'):.2f} "
           f"wait_tmem={frac('mma_wait_tmem'):.2f} wait_sched={frac('mma_wait_sched'):.2f} -> issue-side busy {mma_busy:.2f} | "
