@@ -222,7 +222,8 @@ SD_API uint64_t sd_launch_count(void);
  * 2 no split-K, 4 no heaviest-first row order,
  * 8 backward as two launches instead of one fused launch,
  * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA
- *    (cta_group::2) kernel. */
+ *    (cta_group::2) kernel,
+ * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles. */
 SD_API int sd_set_tuning(int32_t flags);
 
 #ifdef __cplusplus

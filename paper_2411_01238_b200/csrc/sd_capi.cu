@@ -136,6 +136,7 @@ GemmArgs base_args(int rows_out, int cols_out, int red, float scale, void* out) 
     a.out_col_blk = 128;
     a.scale = scale;
     a.out = out;
+    a.keep_hint = -1.0f;
     return a;
 }
 
@@ -679,6 +680,8 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.fwd = prep_dsd_forward(x, mask, w, s, y, y_dtype, m, n, k, nullptr, "layer forward");
         tmp.dw = prep_layer_dw(x, mask, dy, s, dw, dw_dtype, m, n, k);
         tmp.dx = prep_layer_dx(dy, w, mask, s, dx, dx_dtype, m, n, k);
+        // nominal keep fraction: lets the GEMM launcher pick the unit kind (tile shape)
+        tmp.fwd.args.keep_hint = tmp.dw.args.keep_hint = tmp.dx.args.keep_hint = static_cast<float>(1.0 - p);
         require_device();
         cudaGetDevice(&tmp.device);
         (void)sched_slot();  // allocate the scheduler slots now (keeps launches capturable)

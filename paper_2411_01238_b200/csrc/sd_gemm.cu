@@ -15,7 +15,11 @@
 //
 // Tile: 128 output rows (one tcgen05 M=128 MMA, TMEM lanes = rows) x up to 256
 // output columns (MMA N chosen per tile at run time: 256, or 128 for a ragged
-// edge / an odd kept sdd block). Reduction in 64-element stages = one 128-byte
+// edge / an odd kept sdd block), or, in the WIDE instantiation, up to 512
+// columns as two N=256 MMAs sharing each stage's A tile: 20 KB of operands per
+// 1M MACs instead of 24, which matters because these kernels are bound by the
+// chip-wide L2->SM bandwidth (~20 TB/s whatever the TMA box shape,
+// tools/box_bench.cu). Reduction in 64-element stages = one 128-byte
 // swizzle atom; a 128-wide mask block is two stages (the paper's retile(1,2),
 // PAPER.md:149-151). Only kept reduction blocks are ever loaded by TMA.
 //
@@ -26,7 +30,8 @@
 //   warp 3      scheduler (one lane): claims + decodes units
 //   warps 4..7  epilogue: tcgen05.ld -> scale -> bf16/fp32 -> swizzled smem
 //               -> TMA store; all-dropped tiles written as +0.0 directly.
-// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
+// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1
+// (WIDE: one 128x512 accumulator whose halves are released one by one).
 // Scheduling is dynamic: the scheduler warp steals units from a global atomic
 // counter (units ordered heaviest first, grouped for L2 reuse; problem 0 before
 // problem 1) when the producer nears the end of its current unit, decodes them
@@ -72,47 +77,74 @@ namespace {
 #ifndef SD_STAGES
 #define SD_STAGES 4
 #endif
-constexpr int kStages = SD_STAGES;
 #ifndef SD_CLAIM_LEAD
 #define SD_CLAIM_LEAD 6  // stages before a unit's last load at which the next unit is claimed
 #endif
-constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
-constexpr int kBBytes = kBN * kBK * 2;  // 32 KB per stage
+// wide (128 x 512) tiles: separate A / B rings (a 64-deep stage = one A slot +
+// one or two 256-column B slots)
+#ifndef SD_WSTAGES_A
+#define SD_WSTAGES_A 3
+#endif
+#ifndef SD_WSTAGES_B
+#define SD_WSTAGES_B 4
+#endif
+#ifndef SD_CLAIM_LEAD_W
+#define SD_CLAIM_LEAD_W 4
+#endif
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB: one A slot (128 rows x 64)
+constexpr int kBBytes = kBN * kBK * 2;  // 32 KB: one B slot (256 columns x 64)
 constexpr int kEpiWarps = 4;
 constexpr int kEpiBufBytes = 32 * 128;  // one warp's 32 rows x 128 B store box
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
 constexpr int kMaxProblems = 2;
-
-constexpr int kOffA = 0;
-constexpr int kOffB = kOffA + kStages * kABytes;
-constexpr int kOffEpi = kOffB + kStages * kBBytes;
-constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
 constexpr int kGroupRows = 16;  // tile rows per rasterization group
-constexpr int kSchedDepth = 4;  // decoded-unit ring between the producer and the consumers
-constexpr int kNumBars = 2 * kStages + 4 + 2 * kSchedDepth + 1;
-constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
-constexpr int kOffSched = kOffTmemSlot + 16;
+constexpr int kSchedDepth = 4;  // decoded-unit ring between the scheduler and the other roles
+constexpr int kListCap = 64;    // kept-block list entries staged per ring slot (longer lists: __ldg)
 
 struct Unit {
     int prob;      // problem index; -1 = end of work
     int row0;      // first output row
     int list_row;  // mask row (list index) of this tile row
     int n0;        // first output column (dsd)
-    int n_eff;     // MMA N; 0 => no MMA work
+    int n_eff;     // output columns (MMA N; wide: two 256-column halves); 0 => no MMA work
     int nstages;   // reduction stages
     int nslots;    // sdd: kept output blocks in this unit
-    int slot_blk[2];
     int nzero;     // sdd: dropped output blocks in this unit
-    int zero_blk[2];
-    int pad[4];    // pad[0]: dsd first list entry (split-K); pad[1]: unit width (256 or 128 in the tail)
+    int slot_blk[4];
+    int zero_blk[4];
+    int first_entry;  // dsd: first list entry (split-K)
+    int width;        // unit width in columns (zero fill of an all-dropped dsd unit)
+    int pad[6];
 };
-static_assert(sizeof(Unit) == 64, "Unit layout");
+static_assert(sizeof(Unit) == 96, "Unit layout");
 
-constexpr int kListCap = 64;  // kept-block list entries staged per ring slot (longer lists: __ldg)
-constexpr int kOffList = kOffSched + static_cast<int>(sizeof(Unit)) * kSchedDepth;
-constexpr int kSmemBytes = kOffList + kListCap * 4 * kSchedDepth + 1024;  // + align slack
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+// Per-mode kernel configuration.
+//   narrow: 128 x 256 units, a 4-stage ring of {A 16 KB, B 32 KB}, two 128x256
+//           fp32 TMEM accumulators (tile i's epilogue overlaps tile i+1's MMAs)
+//   WIDE:   128 x 512 units: 20 KB of operands per 1M MACs instead of 24 (the
+//           kernels are bound by chip-wide L2->SM bandwidth, tools/box_bench.cu).
+//           An A ring and a B ring of 256-column slots; ONE 128x512 accumulator
+//           whose halves are released to the next unit as the epilogue drains
+//           them. Narrower units (ragged edges) use half 0 only.
+template <bool WIDE>
+struct KCfg {
+    static constexpr int kSA = WIDE ? SD_WSTAGES_A : SD_STAGES;
+    static constexpr int kSB = WIDE ? SD_WSTAGES_B : SD_STAGES;
+    static constexpr int kWidth = WIDE ? 2 * kBN : kBN;
+    static constexpr int kClaimLead = WIDE ? SD_CLAIM_LEAD_W : SD_CLAIM_LEAD;
+    static constexpr int kOffA = 0;
+    static constexpr int kOffB = kOffA + kSA * kABytes;
+    static constexpr int kOffEpi = kOffB + kSB * kBBytes;
+    static constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+    // full[kSB] empty[kSB] aempty[kSA] tfull[2] tempty[2] sfull[D] sempty[D] claim
+    static constexpr int kNumBars = 2 * kSB + kSA + 4 + 2 * kSchedDepth + 1;
+    static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
+    static constexpr int kOffSched = kOffTmemSlot + 16;
+    static constexpr int kOffList = kOffSched + static_cast<int>(sizeof(Unit)) * kSchedDepth;
+    static constexpr int kSmem = kOffList + kListCap * 4 * kSchedDepth + 1024;  // + align slack
+    static_assert(kSmem <= 232448, "shared memory budget");
+};
 
 struct LaunchArgs {
     GemmArgs p[kMaxProblems];
@@ -126,6 +158,7 @@ struct TensorMaps {
     CUtensorMap m[3 * kMaxProblems];  // A, B, Out per problem
 };
 
+template <bool WIDE>
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) {
     Unit t;
     t.prob = prob;
@@ -163,8 +196,9 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
     t.list_row = t.row0 / a.out_row_blk;
     t.nslots = 0;
     t.nzero = 0;
-    const int width = half ? kBN / 2 : kBN;
-    t.pad[1] = width;
+    t.first_entry = 0;
+    const int width = half ? KCfg<WIDE>::kWidth / 2 : KCfg<WIDE>::kWidth;
+    t.width = width;
     if (!(a.flags & kFlagSDD)) {
         t.n0 = cu * width;
         const int rem = a.cols_out - t.n0;
@@ -173,12 +207,12 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         // this split's contiguous share [lo, hi) of the row's kept blocks
         const int lo = static_cast<int>((static_cast<int64_t>(cnt) * split) / a.splits);
         const int hi = static_cast<int>((static_cast<int64_t>(cnt) * (split + 1)) / a.splits);
-        t.pad[0] = lo;  // first list entry
+        t.first_entry = lo;
         t.nstages = (hi - lo) * (a.red_blk / kBK);
         if (hi == lo) t.n_eff = 0;
     } else {
         // Pack the row's KEPT output blocks (compacted list, ascending) into
-        // 256-wide units, so every unit but the row's last runs a full N=256 MMA;
+        // full-width units, so every unit but the row's last runs full-N MMAs;
         // the same unit index also zero-fills the row's DROPPED blocks (kept at
         // the tail of the list by the mask kernel).
         const int per_unit = width / a.out_col_blk;
@@ -197,9 +231,10 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
     return t;
 }
 
+template <bool WIDE>
 __device__ __forceinline__ Unit decode_global(const LaunchArgs& L, int u) {
-    if (L.nprob > 1 && u >= L.p[1].unit_begin) return decode_unit(L.p[1], 1, u - L.p[1].unit_begin);
-    return decode_unit(L.p[0], 0, u);
+    if (L.nprob > 1 && u >= L.p[1].unit_begin) return decode_unit<WIDE>(L.p[1], 1, u - L.p[1].unit_begin);
+    return decode_unit<WIDE>(L.p[0], 0, u);
 }
 
 // Zero a 32-row x `ncols` slab of the output with coalesced 16-byte stores.
@@ -219,7 +254,11 @@ __device__ __forceinline__ void zero_rows(const GemmArgs& a, int row_first, int 
 }
 
 // Epilogue of one unit for one warp (32 output rows).
-template <bool OUT_F32>
+//   narrow: the unit's accumulator is TMEM region (acc_iter & 1), released at the end
+//   WIDE:   columns [0,256) / [256,512) are regions 0 / 1, each released (tempty)
+//           as soon as it is drained, so the next unit's MMAs start on region 0
+//           while region 1 is still being stored
+template <bool WIDE, bool OUT_F32>
 __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorMap* tmOut, const Unit& t,
                                               uint32_t q, uint32_t lane, uint32_t tmem_base,
                                               uint64_t* tfull_bar, uint64_t* tempty_bar, uint8_t* ebuf,
@@ -236,27 +275,50 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
     if (t.n_eff == 0) {
         if (!sdd && !(a.flags & kFlagReduce)) {
             const int rem = a.cols_out - t.n0;
-            const int w = t.pad[1];
+            const int w = t.width;
             if (rem > 0) zero_rows<OUT_F32>(a, row_first, t.n0, rem < w ? rem : w, lane);
         }
         return;
     }
-    const uint32_t acc = acc_iter & 1;
-    const uint32_t acc_phase = (acc_iter >> 1) & 1;
+    uint32_t acc_col0, full_idx, full_phase;
+    if constexpr (WIDE) {
+        acc_col0 = 0;
+        full_idx = 0;
+        full_phase = acc_iter & 1;
+    } else {
+        acc_col0 = (acc_iter & 1) * kBN;
+        full_idx = acc_iter & 1;
+        full_phase = (acc_iter >> 1) & 1;
+    }
     ++acc_iter;
-    SD_TWAIT(5, ptx::mbar_wait(tfull_bar + acc, acc_phase));
+    SD_TWAIT(5, ptx::mbar_wait(tfull_bar + full_idx, full_phase));
     ptx::tc_fence_after();
     const int nchunks = t.n_eff / kChunkCols;
     for (int c = 0; c < nchunks; ++c) {
-        const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kBN + c * kChunkCols;
+        const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc_col0 + c * kChunkCols;
         uint32_t v[kChunkCols];
         ptx::tmem_ld_32x32b_x32(taddr, v);
         if constexpr (!OUT_F32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
         ptx::tmem_ld_wait();
-        if (c == nchunks - 1) {
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty_bar + acc);
+        const bool last = c == nchunks - 1;
+        if constexpr (WIDE) {
+            // region 0 drained (columns [0,256) read out): the next unit may start on it;
+            // region 1 is released at the end of every unit (used or not)
+            const bool end_r0 = (c + 1) * kChunkCols == kBN;
+            if (end_r0 || last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (end_r0 || t.n_eff <= kBN) ptx::mbar_arrive(tempty_bar + 0);
+                    if (last) ptx::mbar_arrive(tempty_bar + 1);
+                }
+            }
+        } else {
+            if (last) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(tempty_bar + full_idx);
+            }
         }
         // staging buffer bi must no longer be read by the TMA store issued 2 chunks ago
         if (lane == 0) ptx::bulk_wait_group_read<1>();
@@ -300,24 +362,27 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
     }
 }
 
+template <bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     sd_gemm_kernel(const __grid_constant__ TensorMaps tms, const __grid_constant__ LaunchArgs L) {
+    using C = KCfg<WIDE>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
     const uint32_t sbase = ptx::smem_u32(smem);
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-    uint64_t* full_bar = bars;
-    uint64_t* empty_bar = bars + kStages;
-    uint64_t* tfull_bar = bars + 2 * kStages;
-    uint64_t* tempty_bar = bars + 2 * kStages + 2;
-    uint64_t* sfull_bar = bars + 2 * kStages + 4;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* full_bar = bars;                 // B slot (+ its stage's A tile) landed
+    uint64_t* empty_bar = bars + C::kSB;       // B slot (narrow: the whole stage) consumed
+    uint64_t* aempty_bar = bars + 2 * C::kSB;  // WIDE: A slot consumed (both halves of its stage)
+    uint64_t* tfull_bar = aempty_bar + C::kSA;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint64_t* sfull_bar = tempty_bar + 2;
     uint64_t* sempty_bar = sfull_bar + kSchedDepth;
     uint64_t* claim_bar = sempty_bar + kSchedDepth;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
-    Unit* sched_unit = reinterpret_cast<Unit*>(smem + kOffSched);
-    int32_t* sched_list = reinterpret_cast<int32_t*>(smem + kOffList);  // [kSchedDepth][kListCap]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmemSlot);
+    Unit* sched_unit = reinterpret_cast<Unit*>(smem + C::kOffSched);
+    int32_t* sched_list = reinterpret_cast<int32_t*>(smem + C::kOffList);  // [kSchedDepth][kListCap]
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
@@ -328,10 +393,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 3 * L.nprob; ++i) ptx::prefetch_tmap(&tms.m[i]);
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < C::kSB; ++i) {
             ptx::mbar_init(full_bar + i, 1);
             ptx::mbar_init(empty_bar + i, 1);
         }
+        for (int i = 0; i < C::kSA; ++i) ptx::mbar_init(aempty_bar + i, 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(tfull_bar + i, 1);
             ptx::mbar_init(tempty_bar + i, kEpiWarps);
@@ -360,17 +426,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
     if (warp == 0) {
-        // ===================== TMA producer (+ scheduler) =====================
+        // ===================== TMA producer =====================
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_normal();
-            int stage = 0;
+            int stage = 0;      // B slot
             uint32_t phase = 0;
+            int sa = 0;         // WIDE: A slot
+            uint32_t pa = 0;
             int sslot = 0;
             uint32_t sphase = 0;
             // Units come from the scheduler warp through the ring; kClaimLead
             // stages before this unit's loads are all issued, the scheduler is
             // told to claim the next one (see warp 3).
-            constexpr int kClaimLead = SD_CLAIM_LEAD;
+            constexpr int kClaimLead = C::kClaimLead;
             while (true) {
                 SD_TWAIT(1, ptx::mbar_wait(sfull_bar + sslot, sphase));
                 const Unit cur = sched_unit[sslot];
@@ -396,9 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool a_mn = a.flags & kFlagAMN;
                 const bool b_mn = a.flags & kFlagBMN;
                 const bool sdd = a.flags & kFlagSDD;
-                const uint32_t tx_bytes = kABytes + cur.n_eff * kBK * 2;
+                const int nh = WIDE ? (cur.n_eff + kBN - 1) / kBN : 1;  // 256-column halves
+                const int per_half = sdd ? kBN / a.out_col_blk : 0;    // sdd blocks per B slot
                 const int spb = a.red_blk / kBK;
-                const int li0 = sdd ? 0 : cur.pad[0];
+                const int li0 = sdd ? 0 : cur.first_entry;
                 const int32_t* lst =
                     (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
                                          : nullptr;
@@ -424,51 +493,60 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         r0 = s * kBK;
                     }
-                    SD_TWAIT(0, ptx::mbar_wait(empty_bar + stage, phase ^ 1));
-                    uint64_t* fb = full_bar + stage;
-#ifdef SD_DIAG_NO_TMA
-                    ptx::mbar_arrive(fb);
-                    (void)tx_bytes;
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                    continue;
-#endif
-                    ptx::mbar_arrive_expect_tx(fb, tx_bytes);
-                    uint8_t* sA = smem + kOffA + stage * kABytes;
-                    uint8_t* sB = smem + kOffB + stage * kBBytes;
-                    if (!a_mn) {
-                        ptx::tma_load_2d(tmA, fb, sA, r0, cur.row0, pol);
-                    } else {
-                        ptx::tma_load_3d(tmA, fb, sA, 0, r0, cur.row0 / 64, pol);
-                    }
-                    if (!sdd) {
-                        if (!b_mn) {
-                            for (int j = 0; j < cur.n_eff / 128; ++j)
-                                ptx::tma_load_2d(tmB, fb, sB + j * 16384, r0, cur.n0 + 128 * j, pol);
-                        } else {
-                            for (int j = 0; j < cur.n_eff / 128; ++j)
-                                ptx::tma_load_3d(tmB, fb, sB + j * 16384, 0, r0, (cur.n0 + 128 * j) / 64, pol);
+                    for (int h = 0; h < nh; ++h) {
+                        const int ncols = WIDE ? min(kBN, cur.n_eff - kBN * h) : cur.n_eff;
+                        uint32_t tx_bytes = static_cast<uint32_t>(ncols) * kBK * 2;
+                        SD_TWAIT(0, ptx::mbar_wait(empty_bar + stage, phase ^ 1));
+                        uint8_t* sA = smem + C::kOffA + (WIDE ? sa : stage) * kABytes;
+                        if (h == 0) {
+                            if constexpr (WIDE) SD_TWAIT(0, ptx::mbar_wait(aempty_bar + sa, pa ^ 1));
+                            tx_bytes += kABytes;
                         }
-                    } else {
-                        for (int sl = 0; sl < cur.nslots; ++sl) {
-                            const int col0 = cur.slot_blk[sl] * a.out_col_blk;
-                            if (!b_mn) {
-                                const int per = a.out_col_blk / 128;
-                                for (int j = 0; j < per; ++j)
-                                    ptx::tma_load_2d(tmB, fb, sB + (sl * per + j) * 16384, r0, col0 + 128 * j, pol);
-                            } else {
-                                const int per = a.out_col_blk / 128;
-                                for (int j = 0; j < per; ++j)
-                                    ptx::tma_load_3d(tmB, fb, sB + (sl * per + j) * 16384, 0, r0, (col0 + 128 * j) / 64,
-                                                     pol);
+                        uint64_t* fb = full_bar + stage;
+#ifdef SD_DIAG_NO_TMA
+                        ptx::mbar_arrive(fb);
+                        (void)tx_bytes;
+                        (void)per_half;
+                        (void)sA;
+#else
+                        ptx::mbar_arrive_expect_tx(fb, tx_bytes);
+                        if (h == 0) {
+                            if (!a_mn) ptx::tma_load_2d(tmA, fb, sA, r0, cur.row0, pol);
+                            else ptx::tma_load_3d(tmA, fb, sA, 0, r0, cur.row0 / 64, pol);
+                        }
+                        uint8_t* sB = smem + C::kOffB + stage * kBBytes;
+                        if (!sdd) {
+                            const int c0 = cur.n0 + kBN * h;
+                            for (int j = 0; j < ncols / 128; ++j) {
+                                if (!b_mn) ptx::tma_load_2d(tmB, fb, sB + j * 16384, r0, c0 + 128 * j, pol);
+                                else ptx::tma_load_3d(tmB, fb, sB + j * 16384, 0, r0, (c0 + 128 * j) / 64, pol);
+                            }
+                        } else {
+                            const int per = a.out_col_blk / 128;
+                            const int sl_end = min(cur.nslots, (h + 1) * per_half);
+                            for (int sl = h * per_half; sl < sl_end; ++sl) {
+                                const int col0 = cur.slot_blk[sl] * a.out_col_blk;
+                                const int off = (sl - h * per_half) * per;
+                                for (int j = 0; j < per; ++j) {
+                                    if (!b_mn)
+                                        ptx::tma_load_2d(tmB, fb, sB + (off + j) * 16384, r0, col0 + 128 * j, pol);
+                                    else
+                                        ptx::tma_load_3d(tmB, fb, sB + (off + j) * 16384, 0, r0, (col0 + 128 * j) / 64,
+                                                         pol);
+                                }
                             }
                         }
+#endif
+                        if (++stage == C::kSB) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
+                    if constexpr (WIDE) {
+                        if (++sa == C::kSA) {
+                            sa = 0;
+                            pa ^= 1;
+                        }
                     }
                 }
                 ptx::mbar_arrive(sempty_bar + cur_slot);  // done with the slot's staged list
@@ -493,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (true) {
             Unit t;
             if (lane == 0) {
-                if (u < num_units) t = decode_global(L, u); else t.prob = -1;
+                if (u < num_units) t = decode_global<WIDE>(L, u); else t.prob = -1;
             }
             // list source of this unit (dsd with a list): entries [li0, li0 + nblk)
             const int32_t* src = nullptr;
@@ -501,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0 && t.prob >= 0 && t.n_eff > 0) {
                 const GemmArgs& a = L.p[t.prob];
                 if (!(a.flags & kFlagSDD) && a.list_idx) {
-                    src = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride + t.pad[0];
+                    src = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride + t.first_entry;
                     nblk = t.nstages / (a.red_blk / kBK);
                 }
             }
@@ -532,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            int sa = 0;
             uint32_t acc_iter = 0;
             int sslot = 0;
             uint32_t sphase = 0;
@@ -548,38 +627,83 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const GemmArgs& a = L.p[t.prob];
                 const bool a_mn = a.flags & kFlagAMN;
                 const bool b_mn = a.flags & kFlagBMN;
-                const uint32_t acc = acc_iter & 1;
-                const uint32_t acc_phase = (acc_iter >> 1) & 1;
-                ++acc_iter;
-                SD_TWAIT(3, ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1));
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * kBN;
-                const uint32_t idesc = ptx::make_idesc_bf16(kBM, t.n_eff, a_mn, b_mn);
                 const uint32_t a_step = a_mn ? 2048u : 32u, b_step = b_mn ? 2048u : 32u;
                 const uint32_t a_lbo = a_mn ? 8192u : 0u, b_lbo = b_mn ? 8192u : 0u;
-                for (int s = 0; s < t.nstages; ++s) {
-                    SD_TWAIT(2, ptx::mbar_wait(full_bar + stage, phase));
-                    SD_TADD(8, 1);
+                if constexpr (!WIDE) {
+                    const uint32_t acc = acc_iter & 1;
+                    const uint32_t acc_phase = (acc_iter >> 1) & 1;
+                    ++acc_iter;
+                    SD_TWAIT(3, ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1));
                     ptx::tc_fence_after();
-                    const uint32_t a_addr = sbase + kOffA + stage * kABytes;
-                    const uint32_t b_addr = sbase + kOffB + stage * kBBytes;
+                    const uint32_t d_tmem = tmem_base + acc * kBN;
+                    const uint32_t idesc = ptx::make_idesc_bf16(kBM, t.n_eff, a_mn, b_mn);
+                    for (int s = 0; s < t.nstages; ++s) {
+                        SD_TWAIT(2, ptx::mbar_wait(full_bar + stage, phase));
+                        SD_TADD(8, 1);
+                        ptx::tc_fence_after();
+                        const uint32_t a_addr = sbase + C::kOffA + stage * kABytes;
+                        const uint32_t b_addr = sbase + C::kOffB + stage * kBBytes;
 #ifndef SD_DIAG_NO_MMA
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
-                        const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
-                        ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
-                    }
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                            const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
+                            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                        }
 #else
-                    (void)a_addr; (void)b_addr; (void)idesc; (void)a_step; (void)b_step; (void)a_lbo; (void)b_lbo;
+                        (void)a_addr; (void)b_addr; (void)idesc; (void)a_step; (void)b_step; (void)a_lbo; (void)b_lbo;
 #endif
-                    ptx::mma_commit(empty_bar + stage);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
+                        ptx::mma_commit(empty_bar + stage);
+                        if (++stage == C::kSB) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
+                    ptx::mma_commit(tfull_bar + acc);
+                } else {
+                    // one 128 x 512 accumulator: half h = TMEM columns [256h, 256h + 256)
+                    const int nh = (t.n_eff + kBN - 1) / kBN;
+                    const uint32_t rphase = acc_iter & 1;
+                    ++acc_iter;
+                    SD_TWAIT(3, ptx::mbar_wait(tempty_bar + 0, rphase ^ 1));
+                    ptx::tc_fence_after();
+                    const uint32_t idesc0 = ptx::make_idesc_bf16(kBM, min(kBN, t.n_eff), a_mn, b_mn);
+                    const uint32_t idesc1 = ptx::make_idesc_bf16(kBM, max(16, t.n_eff - kBN), a_mn, b_mn);
+                    for (int s = 0; s < t.nstages; ++s) {
+                        const uint32_t a_addr = sbase + C::kOffA + sa * kABytes;
+                        for (int h = 0; h < nh; ++h) {
+                            if (h == 1 && s == 0) {
+                                // half 1: free once the previous unit's epilogue drained it
+                                SD_TWAIT(3, ptx::mbar_wait(tempty_bar + 1, rphase ^ 1));
+                                ptx::tc_fence_after();
+                            }
+                            SD_TWAIT(2, ptx::mbar_wait(full_bar + stage, phase));
+                            SD_TADD(8, 1);
+                            ptx::tc_fence_after();
+                            const uint32_t b_addr = sbase + C::kOffB + stage * kBBytes;
+#ifndef SD_DIAG_NO_MMA
+#pragma unroll
+                            for (int k = 0; k < kBK / 16; ++k) {
+                                const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                                const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
+                                ptx::mma_bf16_ss(tmem_base + kBN * h, ad, bd, h ? idesc1 : idesc0,
+                                                 (s > 0 || k > 0) ? 1u : 0u);
+                            }
+#else
+                            (void)a_addr; (void)b_addr; (void)idesc0; (void)idesc1; (void)a_step; (void)b_step; (void)a_lbo;
+                            (void)b_lbo;
+#endif
+                            ptx::mma_commit(empty_bar + stage);
+                            if (++stage == C::kSB) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                        ptx::mma_commit(aempty_bar + sa);
+                        if (++sa == C::kSA) sa = 0;
+                    }
+                    ptx::mma_commit(tfull_bar + 0);
                 }
-                ptx::mma_commit(tfull_bar + acc);
                 if (a.counters)
                     atomicAdd(a.counters + t.row0 / kBM,
                               static_cast<unsigned long long>(t.nstages / 2) * (t.n_eff / 128));
@@ -588,8 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ===================== epilogue =====================
         const uint32_t q = warp & 3;  // TMEM lane quarter == output row quarter
-        uint8_t* ebuf = smem + kOffEpi + q * 2 * kEpiBufBytes;
-        const uint32_t ebuf_addr = sbase + kOffEpi + q * 2 * kEpiBufBytes;
+        uint8_t* ebuf = smem + C::kOffEpi + q * 2 * kEpiBufBytes;
+        const uint32_t ebuf_addr = sbase + C::kOffEpi + q * 2 * kEpiBufBytes;
         uint32_t bi = 0;
         uint32_t acc_iter = 0;
         int sslot = 0;
@@ -607,11 +731,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const GemmArgs& a = L.p[t.prob];
             const CUtensorMap* tmOut = &tms.m[3 * t.prob + 2];
             if (a.flags & kFlagF32)
-                epilogue_unit<true>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr, bi,
-                                    acc_iter, tr);
+                epilogue_unit<WIDE, true>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr,
+                                          bi, acc_iter, tr);
             else
-                epilogue_unit<false>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr, bi,
-                                     acc_iter, tr);
+                epilogue_unit<WIDE, false>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr,
+                                           bi, acc_iter, tr);
             SD_TADD(11, 1);
         }
         if (lane == 0) ptx::bulk_wait_group<0>();
@@ -663,16 +787,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Scheduler tuning switches (A/B experiments). Tail halving is off by default:
 // interleaved A/B (tools/ab_tuning.py) showed half-width tail units cost more in
 // operand ingress than they save in idle tail (4096^3: +4% at p=0.5, +11% at p=0.1).
-static int g_tuning = kTuneNoTailHalving;
+// SD_TUNING (environment) overrides the default for whole-process A/B runs.
+static int initial_tuning() {
+    const char* e = std::getenv("SD_TUNING");
+    return e ? std::atoi(e) : kTuneNoTailHalving;
+}
+static int g_tuning = initial_tuning();
 int tuning() { return g_tuning; }
 void set_tuning(int t) { g_tuning = t; }
+
+// Unit width of a launch. 128 x 512 units cut operand bytes per MAC by a sixth
+// but hold the whole TMEM (no second accumulator to overlap the epilogue
+// with). Measured in one process on the same buffers (tools/ab_libs.py, one
+// B200): dsd forward 2-6% faster at 4096^3-8192^3 for p <= 0.5, dW within +-2%,
+// sdd (dX) 4-8% slower, and near p = 0.9 the units get too short (+30-45%). So:
+// wide for launches of dsd problems only, with 512+ columns, unless the mask
+// keeps under 20%; no keep hint (generic C-ABI calls) counts as dense enough.
+static bool wide_units(const GemmCall* const* calls, int n) {
+    if (g_tuning & kTuneNarrow) return false;
+    if (g_tuning & kTuneWide) return true;
+    for (int i = 0; i < n; ++i) {
+        const GemmArgs& a = calls[i]->args;
+        if ((a.flags & kFlagSDD) || a.cols_out <= kBN) return false;
+        if (a.keep_hint >= 0.f && a.keep_hint < 0.2f) return false;
+    }
+    return true;
+}
 
 void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
     static bool configured = false;
     if (!configured) {
-        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes),
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        KCfg<false>::kSmem),
                    "cudaFuncSetAttribute(max dynamic smem)");
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        KCfg<true>::kSmem),
+                   "cudaFuncSetAttribute(max dynamic smem, wide)");
         configured = true;
     }
     // dense problems go to the 2-CTA kernel (half the per-SM operand traffic
@@ -698,16 +849,22 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     // the MLP's dW, 72 tiles over a 65536-long reduction): fp32 outputs only,
     // partial sums reduce-added by TMA into the zeroed output (the summation
     // order across splits is then not fixed; results stay within tolerance).
+    // unit width: 128 x 512 (wide) or 128 x 256, one choice per launch
+    const bool wide = wide_units(calls, n);
+    const int width = wide ? 2 * kBN : kBN;
     GemmArgs pa[kMaxProblems];
     float cost[kMaxProblems];
     for (int i = 0; i < n; ++i) {
         pa[i] = calls[i]->args;
         pa[i].splits = 1;
         pa[i].tail_rows = 0;
+        pa[i].n_col_units = (pa[i].cols_out + width - 1) / width;
         const int base = pa[i].n_row_tiles * pa[i].n_col_units;
         const bool sdd = pa[i].flags & kFlagSDD;
         const int red_stages = pa[i].red / kBK;
-        if (!(g_tuning & kTuneNoSplitK) && !sdd && (pa[i].flags & kFlagF32) && base < 2 * sms && red_stages >= 64) {
+        const int split_below = wide ? sms : 2 * sms;  // a wide unit carries two narrow units' work
+        if (!(g_tuning & kTuneNoSplitK) && !sdd && (pa[i].flags & kFlagF32) && base < split_below &&
+            red_stages >= 64) {
             int sp = (2 * sms + base - 1) / base;
             sp = std::min(sp, red_stages / 32);
             if (sp > 1) {
@@ -737,7 +894,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
         for (int i = 0; i < n; ++i) total_units += gemm_units(pa[i]);
         GemmArgs& last = pa[order[n - 1]];
         const bool sdd = last.flags & kFlagSDD;
-        if (!(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units < 12 * sms &&
+        if (!wide && !(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units < 12 * sms &&
             (!sdd || last.out_col_blk == 128)) {
             const int T = (sms + last.n_col_units - 1) / last.n_col_units;
             last.tail_rows = std::min(T, last.n_row_tiles);
@@ -768,14 +925,15 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = wide ? KCfg<true>::kSmem : KCfg<false>::kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel, tms, L), "sd_gemm_kernel launch");
+    if (wide) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<true>, tms, L), "sd_gemm_kernel<wide> launch");
+    else check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<false>, tms, L), "sd_gemm_kernel launch");
     note_launch();
 }
 

@@ -68,6 +68,7 @@ struct GemmArgs {
     unsigned long long* counters;
     int splits;        // dsd split-K factor (>= 1): each unit reduces a contiguous 1/splits of its list
     int tail_rows;     // the last tail_rows tile rows (lightest, end of the queue) use half-width units
+    float keep_hint;   // nominal kept fraction of the mask (1 - p) when known, else < 0
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
@@ -94,6 +95,8 @@ enum TuneFlags : int {
     kTuneNoRowOrder = 4,
     kTuneNoFusedBackward = 8,
     kTuneNoGemm2 = 16,  // dense problems on the 1-CTA kernel instead of the 2-CTA one
+    kTuneWide = 32,     // force 128 x 512 units on the 1-CTA kernel
+    kTuneNarrow = 64,   // force 128 x 256 units on the 1-CTA kernel
 };
 int tuning();
 void set_tuning(int t);

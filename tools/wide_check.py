@@ -1,0 +1,66 @@
+"""128x512 (wide) vs 128x256 tiles: bitwise equality of every GEMM of the layer
+path and A/B timing (dev tool). python tools/wide_check.py"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_01238_b200 as sd  # noqa: E402
+
+lib = sd.load_library()
+NORMAL, WIDE = 0, 32
+TUNINGS = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [NORMAL, WIDE]
+
+
+def layer_outputs(plan, seed):
+    plan.forward(seed)
+    plan.backward()
+    torch.cuda.synchronize()
+    return [t.clone() for t in (plan.y, plan.dx, plan.dw)]
+
+
+shapes = [(1024, 1024, 1024, 0.5), (4096, 4096, 4096, 0.5), (4096, 4096, 4096, 0.1), (2048, 768, 3072, 0.3),
+          (2048, 3072, 768, 0.5), (4096, 4096, 4096, 0.9), (1024, 640, 1152, 0.5), (8192, 8192, 8192, 0.5),
+          (8192, 8192, 8192, 0.1), (65536, 768, 3072, 0.5), (65536, 3072, 768, 0.5)]
+ok = True
+for (M, N, K, p) in shapes:
+    x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    plan = sd.LayerPlan(x, w, dy, p)
+    lib.sd_set_tuning(NORMAL)
+    a = layer_outputs(plan, 7)
+    for tv in TUNINGS[1:]:
+        lib.sd_set_tuning(tv)
+        b = layer_outputs(plan, 7)
+        same = [torch.equal(u, v) for u, v in zip(a, b)]
+        if not same[2]:  # split-K dW (reduce-add order) differs in rounding only
+            same[2] = bool(((a[2].float() - b[2].float()).abs().max() <= 1e-5 * a[2].float().abs().max()).item())
+        print(f"M={M} N={N} K={K} p={p} tuning {tv}: y/dx/dw bitwise equal to tuning {NORMAL}: {same}", flush=True)
+        ok = ok and all(same)
+    if M >= 4096:
+        for tune in TUNINGS:
+            lib.sd_set_tuning(tune)
+            for _ in range(5):
+                plan.forward(1); plan.backward()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            n = 20
+            ev[0].record()
+            for i in range(n):
+                plan.forward(i)
+            ev[1].record()
+            for i in range(n):
+                plan.backward()
+            ev[2].record()
+            for i in range(n):
+                plan.backward_dw()
+            ev[3].record()
+            for i in range(n):
+                plan.backward_dx()
+            ev[4].record()
+            torch.cuda.synchronize()
+            t = [ev[j].elapsed_time(ev[j + 1]) / n * 1e3 for j in range(4)]
+            print(f"   tuning={tune}: fwd {t[0]:.1f} us  bwd {t[1]:.1f} us  (dw {t[2]:.1f}, dx {t[3]:.1f})", flush=True)
+lib.sd_set_tuning(1)
+print("ALL EQUAL" if ok else "MISMATCH")
