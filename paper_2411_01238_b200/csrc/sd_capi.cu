@@ -621,6 +621,27 @@ int sd_dsd_matmul(const void* a, const sd_block_mask* mask, const void* b, float
     });
 }
 
+// Development entry (not in the public header): a dsd GEMM on the 2-CTA kernel
+// in union mode, from caller-built pair lists ((block << 2) | owner bits per
+// 256-row pair). a_mn selects the dW operand layout (A = X read MN-major).
+SD_API int sd_dev_dsd_pairs(const void* a, const void* b, void* c, int32_t c_dtype, int32_t m, int32_t n, int32_t k,
+                            int32_t a_mn, int32_t red_blk, const int32_t* pair_cnt, const int32_t* pair_idx,
+                            int32_t pair_stride, float scale, void* stream) {
+    return guarded([&] {
+        check_gemm(m, n, k);
+        GemmCall g;
+        g.ta = a_mn ? mnmajor_map(a, m, k) : kmajor_map(a, k, m);
+        g.tb = mnmajor_map(b, n, k);
+        g.tout = out_map(c, c_dtype, m, n);
+        g.args = base_args(m, n, k, scale, c);
+        g.args.flags = flags_of(a_mn != 0, true, false, c_dtype);
+        g.args.red_blk = red_blk;
+        if (!gemm2_supported(g.args)) fail(SD_EINVAL, "sd_dev_dsd_pairs: unsupported shape");
+        require_device();
+        launch_gemm2(g.ta, g.tb, g.tout, g.args, pair_cnt, pair_idx, pair_stride, as_stream(stream));
+    });
+}
+
 int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
                       int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
     return guarded([&] {

@@ -14,10 +14,10 @@
 //   TMEM empty      leader only; all 8 epilogue warps of the pair arrive
 // Union mode (dsd with a list per 128-row block): the pair's two row blocks
 // walk the UNION of their kept lists; a CTA whose own row dropped a block
-// zero-fills its A stage instead of loading it, so the dropped block still
-// contributes exact zeros (no wrong results, only redundant MMA work). Used
-// when the mask keeps most blocks (low p), where halving ingress beats the
-// extra MMA work.
+// loads an all-out-of-bounds box instead (TMA zero fill, no memory traffic), so
+// the dropped block still contributes exact zeros (no wrong results, only
+// redundant MMA work) and the accumulation order of every kept product is the
+// 1-CTA kernel's.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -182,28 +182,19 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                     ptx::mbar_wait(empty_bar + stage, phase ^ 1);
                     uint8_t* sA = smem + kOffA + stage * kHalfBytes;
                     uint8_t* sB = smem + kOffB + stage * kHalfBytes;
-                    const uint32_t my_bytes = (own ? kHalfBytes : 0) + kHalfBytes;
-                    if (!own) {
-                        // own row dropped this block: exact zeros into the A half
-                        // (generic-proxy stores made visible to the tensor core)
-                        uint4* z = reinterpret_cast<uint4*>(sA);
-                        for (int i = 0; i < kHalfBytes / 16; ++i) z[i] = make_uint4(0, 0, 0, 0);
-                        ptx::fence_proxy_async_smem();
-                    }
                     if (leader) {
-                        // expect both CTAs' bytes: peer's own-ness comes from the same entry
-                        const bool peer_own = unioned ? ((entry >> 1) & 1) : true;
-                        const uint32_t peer_bytes = (peer_own ? kHalfBytes : 0) + kHalfBytes;
-                        ptx::mbar_arrive_expect_tx(full_bar + stage, my_bytes + peer_bytes);
+                        // both CTAs' A and B halves (a dropped A half is a zero-filled box, same bytes)
+                        ptx::mbar_arrive_expect_tx(full_bar + stage, 4 * kHalfBytes);
                     } else {
                         ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(full_bar + stage), 0));
                     }
-                    if (own) {
-                        if (!a_mn) {
-                            tma_load_2sm(&tmA, full_bar + stage, sA, r0, row0);
-                        } else {
-                            tma_load_2sm_3d(&tmA, full_bar + stage, sA, 0, r0, row0 / 64);
-                        }
+                    // own row dropped this block: load a box lying wholly past the last
+                    // row instead; TMA fills it with exact zeros without touching memory
+                    const int arow = own ? row0 : a.rows_out;
+                    if (!a_mn) {
+                        tma_load_2sm(&tmA, full_bar + stage, sA, r0, arow);
+                    } else {
+                        tma_load_2sm_3d(&tmA, full_bar + stage, sA, 0, r0, arow / 64);
                     }
                     if (!b_mn) {
                         tma_load_2sm(&tmB, full_bar + stage, sB, r0, col0);
