@@ -1,0 +1,161 @@
+"""Kernel-mode parity (GPU): every unit kind / kernel instantiation of the GEMM
+path must produce BIT-IDENTICAL outputs — they reduce each output element over
+the same 16-deep MMA steps in the same order and differ only in tiling:
+
+  narrow  sd_gemm_kernel<false>: 128 x 256 units, double-buffered TMEM
+  wide    sd_gemm_kernel<true>:  128 x 512 units (two N=256 MMAs per A tile)
+  union   sd_gemm2_kernel union mode: 2-CTA pairs over the union of two rows'
+          kept lists, a dropped A half loaded as an out-of-bounds (zero) box
+
+plus one oracle check of the wide path (gemm.hpp:133-213 semantics)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+NARROW, WIDE = 1 | 64, 1 | 32  # sd_set_tuning bits (include/sparsedrop_b200.h)
+
+
+@pytest.fixture(scope="module")
+def sd():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2411_01238_b200 as sd
+
+    sd.load_library()
+    return sd
+
+
+def _dev(o, r, c, seed):
+    return torch.from_numpy(o.random_matrix(r, c, seed)).to(torch.bfloat16).cuda()
+
+
+def _layer_outputs(sd, x, w, dy, p, seed, fused=True):
+    plan = sd.LayerPlan(x, w, dy, p)
+    plan.forward(seed)
+    if fused:
+        plan.backward()
+    else:
+        plan.backward_dw()
+        plan.backward_dx()
+    torch.cuda.synchronize()
+    return [plan.y.clone(), plan.dx.clone(), plan.dw.clone()]
+
+
+# (M, N, K, p): square, ragged N (640 = 512 + 128), narrow N (<= 256 -> narrow
+# even when wide is forced), MLP-like small dW outputs (split-K), p = 0.9 with
+# fully dropped rows, p = 0
+LAYER_CASES = [(1024, 1024, 1024, 0.5), (1024, 640, 1152, 0.3), (512, 256, 768, 0.5), (4096, 768, 384, 0.1),
+               (2048, 3072, 768, 0.9), (1024, 1536, 512, 0.0)]
+
+
+@pytest.mark.parametrize("M,N,K,p", LAYER_CASES)
+@pytest.mark.parametrize("fused", [True, False])
+def test_layer_wide_equals_narrow_bitwise(sd, oracle, M, N, K, p, fused):
+    lib = sd.load_library()
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    try:
+        lib.sd_set_tuning(NARROW)
+        ref = _layer_outputs(sd, x, w, dy, p, 21, fused)
+        lib.sd_set_tuning(WIDE)
+        got = _layer_outputs(sd, x, w, dy, p, 21, fused)
+    finally:
+        lib.sd_set_tuning(1)
+    for name, a, b in zip(("y", "dx", "dw"), ref, got):
+        if name == "dw" and not torch.equal(a, b):
+            # split-K dW (small outputs) reduce-adds partials in arrival order:
+            # identical up to fp32 rounding of the partial sums only
+            assert torch.allclose(a, b, rtol=1e-5, atol=1e-5 * float(a.abs().max())), name
+        else:
+            assert torch.equal(a, b), name
+
+
+@pytest.mark.parametrize("n_blk", [128, 256])
+def test_generic_sdd_and_dsd_wide_equals_narrow(sd, oracle, n_blk):
+    """The generic C-ABI dsd / sdd entry points (reference TileConfig forms)."""
+    lib = sd.load_library()
+    M, N, K = 1024, 1024, 768
+    a, b = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2)
+    m_dsd = sd.sample_mask(sd.DropoutSpec(0.4, 128, 128, 5), M, K)
+    m_sdd = sd.sample_mask(sd.DropoutSpec(0.4, 128, n_blk, 6), M, N)
+    outs = {}
+    try:
+        for tune in (NARROW, WIDE):
+            lib.sd_set_tuning(tune)
+            outs[tune] = (sd.dsd_matmul(a, m_dsd, b, 1.5, out_dtype=torch.float32),
+                          sd.sdd_matmul(a, b, m_sdd, 1.5, out_dtype=torch.bfloat16))
+        torch.cuda.synchronize()
+    finally:
+        lib.sd_set_tuning(1)
+    for u, v in zip(outs[NARROW], outs[WIDE]):
+        assert torch.equal(u, v)
+
+
+def test_wide_forward_matches_oracle(sd, oracle):
+    lib = sd.load_library()
+    M, N, K, p = 512, 1280, 640, 0.5
+    x, w = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2)
+    m = sd.sample_mask(sd.DropoutSpec(p, 128, 128, 3), M, K)
+    s = sd.dropout_scale(p)
+    try:
+        lib.sd_set_tuning(WIDE)
+        y = sd.dsd_matmul(x, m, w, s, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+    finally:
+        lib.sd_set_tuning(1)
+    words = np.array(m.words(), dtype=np.uint64)
+    xn, wn = x.double().cpu().numpy(), w.double().cpu().numpy()
+    ref = oracle.dsd_matmul(xn, words, wn, 128, 128, 128, s)
+    bound = s * (np.abs(xn) @ np.abs(wn))
+    got = y.double().cpu().numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
+    assert (np.abs(got - ref) <= 1e-5 * bound + 1e-30).all()
+
+
+def _pair_lists(bits):
+    """Pairs of rows (2p, 2p+1) of a (R, C) keep matrix -> union lists of
+    (block << 2) | owner bits, the 2-CTA kernel's union-mode format."""
+    R, C = bits.shape
+    cnt = np.zeros(R // 2, np.int32)
+    idx = np.zeros((R // 2, C), np.int32)
+    for q in range(R // 2):
+        own = bits[2 * q].astype(np.int32) | (bits[2 * q + 1].astype(np.int32) << 1)
+        cols = np.nonzero(own)[0]
+        cnt[q] = len(cols)
+        idx[q, :len(cols)] = (cols << 2) | own[cols]
+    return torch.from_numpy(cnt).cuda(), torch.from_numpy(idx).cuda()
+
+
+@pytest.mark.parametrize("p", [0.3, 0.8])
+def test_union_2cta_dsd_bitwise(sd, oracle, p):
+    """2-CTA union mode (dev entry sd_dev_dsd_pairs): a CTA whose row dropped a
+    block multiplies an all-zero (out-of-bounds) A box, so every output equals
+    the 1-CTA dsd bit for bit — forward (row pairs) and dW (mask-column pairs)."""
+    lib = sd.load_library()
+    lib.sd_dev_dsd_pairs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                     ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_float, ctypes.c_void_p]
+    M, N, K = 2048, 1024, 1536
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    plan = sd.LayerPlan(x, w, dy, p)
+    plan.forward(77)
+    plan.backward_dw()
+    torch.cuda.synchronize()
+    R, C = M // 128, K // 128
+    words = np.array(plan.mask.words(), dtype=np.uint64)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: R * C].astype(bool).reshape(R, C)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    fc, fi = _pair_lists(bits)
+    y2 = torch.empty_like(plan.y)
+    assert lib.sd_dev_dsd_pairs(x.data_ptr(), w.data_ptr(), y2.data_ptr(), 1, M, N, K, 0, 128, fc.data_ptr(),
+                                fi.data_ptr(), C, plan.scale, st) == 0
+    dc, di = _pair_lists(bits.T.copy())
+    dw2 = torch.empty_like(plan.dw)
+    assert lib.sd_dev_dsd_pairs(x.data_ptr(), dy.data_ptr(), dw2.data_ptr(), 0, K, N, M, 1, 128, dc.data_ptr(),
+                                di.data_ptr(), R, plan.scale, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y2, plan.y)
+    assert torch.equal(dw2, plan.dw)
