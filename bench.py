@@ -422,6 +422,14 @@ def main():
 
     # ---- dense baseline (same kernel, no mask) and cuBLAS for context
     ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup)
+    # the same dense step on the 1-CTA tile machinery the masked GEMMs use
+    # (tuning 1|16: no 2-CTA kernel) — the like-for-like (1-p) reference
+    _lib_t = sd.load_library()
+    _lib_t.sd_set_tuning(1 | 16)
+    try:
+        ms_dense_1cta = time_steps(dense_step_fn(), args.steps, args.warmup)
+    finally:
+        _lib_t.sd_set_tuning(1)
     ms_torch = time_steps(torch_step, args.steps, args.warmup)
 
     # ---- per-kernel durations at the headline p (roofline): each kernel run
@@ -509,6 +517,7 @@ def main():
                 "dense_equiv_tflops": world * flops_dense_step / (msp * 1e-3) / 1e12,
                 "executed_tflops": world * kp * flops_dense_step / (msp * 1e-3) / 1e12,
                 "speedup_vs_dense": ms_dense / msp,
+                "speedup_vs_dense_1cta": ms_dense_1cta / msp,
                 "time_vs_dense_over_keep": (msp / ms_dense) / max(kp, 1e-9),
             })
             if p != args.p:
@@ -596,6 +605,9 @@ def main():
             "config": workload_config(S, args.p, world),
             "keep_fraction": keep, "executed_tflops": value * keep,
             "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
+            "dense_1cta_ms_per_step": ms_dense_1cta, "speedup_vs_dense_1cta": ms_dense_1cta / ms,
+            "dense_note": ("dense_ms_per_step: our 2-CTA (cta_group::2) dense kernel, the speed-up denominator; "
+                           "dense_1cta_ms_per_step: the same dense step on the 1-CTA tiles the masked GEMMs use"),
             "isolated_ms_per_step": ms_isolated,
             "timing": (f"{n_sets} rotating input sets ({n_sets * set_bytes / 2**20:.0f} MiB > L2), steps back-to-back, "
                        "one CUDA-event pair around the K timed steps; isolated_ms_per_step: one step at a time "
