@@ -54,12 +54,14 @@ def parse_args():
     ap.add_argument("--rotate", type=int, default=3,
                     help="input sets cycled step to step (their combined size exceeds L2, so steps run "
                          "back-to-back without an L2 flush)")
+    ap.add_argument("--dw-parts", type=int, default=2,
+                    help="N>1: dW computed in this many row slabs, each all-reduced while the next slab and dX run")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (CI check of the data-parallel path)")
     return ap.parse_args()
 
 
-def workload_config(size, p, world):
+def workload_config(size, p, world, dw_parts=2):
     return {
         "workload": f"configs[1]: SparseDrop linear fwd+bwd (mask gen + dsd fwd + dsd dW + sdd dX), "
                     f"M={size}/GPU, N=K={size}, 128x128 blocks, p={p} (sweep p=0..0.9 in 'sweep')",
@@ -68,7 +70,8 @@ def workload_config(size, p, world):
         "dtypes": {"x/w/dy/y/dx": "bf16", "dw": "fp32", "accumulate": "fp32"},
         "l2": "inputs larger than L2: steps rotate over several input sets whose combined footprint exceeds "
               "the 126 MB L2 (see 'timing')",
-        "parallelism": f"dp{world} row-sharded (shard-local masks, dW all-reduce)" if world > 1 else "single GPU",
+        "parallelism": (f"dp{world} row-sharded (shard-local masks, dW all-reduced in {max(1, dw_parts)} row "
+                        "slabs overlapping the next slab and dX)") if world > 1 else "single GPU",
     }
 
 
@@ -364,10 +367,14 @@ def main():
             plan = pls[i % n_sets]
             plan.forward(seed=sd.effective_seed(0, i, 0))
             if world > 1:
-                plan.backward_dw()
-                comm.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(comm):
-                    dist.all_reduce(plan.dw)
+                # dW slab by slab: each slab's all-reduce (comm stream) overlaps
+                # the next slab and dX on the compute stream
+                nparts = max(1, args.dw_parts)
+                for part in range(nparts):
+                    slab = plan.backward_dw_part(part, nparts) if nparts > 1 else plan.backward_dw()
+                    comm.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(comm):
+                        dist.all_reduce(slab)
                 plan.backward_dx()
                 torch.cuda.current_stream().wait_stream(comm)
             else:
@@ -602,7 +609,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random_matrix distribution, on device)",
-            "config": workload_config(S, args.p, world),
+            "config": workload_config(S, args.p, world, args.dw_parts),
             "keep_fraction": keep, "executed_tflops": value * keep,
             "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
             "dense_1cta_ms_per_step": ms_dense_1cta, "speedup_vs_dense_1cta": ms_dense_1cta / ms,

@@ -180,6 +180,11 @@ SD_API int sd_layer_plan_create(sd_layer_plan** plan, const void* x, const void*
                                 const sd_block_mask* mask);
 SD_API int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream);
 SD_API int sd_layer_plan_backward(sd_layer_plan* plan, void* stream);
+/* dW rows of mask-column blocks [C*part/nparts, C*(part+1)/nparts) only — the
+ * same tiles and reduction order as sd_layer_plan_backward_dw, so the parts
+ * together equal it bit for bit. Data-parallel callers all-reduce each part
+ * while the next part and dX compute. SD_ERANGE for a bad part/nparts. */
+SD_API int sd_layer_plan_backward_dw_part(sd_layer_plan* plan, int32_t part, int32_t nparts, void* stream);
 SD_API int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream);
 SD_API int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream);
 /* Dense baseline with the same buffers (layer.hpp:98-99, 140-145): y = x w,

@@ -483,6 +483,13 @@ class LayerPlan:
         check(_lib().sd_layer_plan_backward_dw(self._plan, ctypes.c_void_p(_stream(stream))))
         return self.dw
 
+    def backward_dw_part(self, part: int, nparts: int, stream=None):
+        """dW rows of mask-column blocks [C*part/nparts, C*(part+1)/nparts): returns
+        that row slab of self.dw (bit-identical to the same rows of backward_dw)."""
+        check(_lib().sd_layer_plan_backward_dw_part(self._plan, part, nparts, ctypes.c_void_p(_stream(stream))))
+        C, kb = self.mask.block_cols(), self.mask.k_blk()
+        return self.dw[(C * part // nparts) * kb:(C * (part + 1) // nparts) * kb]
+
     def backward_dx(self, stream=None):
         check(_lib().sd_layer_plan_backward_dx(self._plan, ctypes.c_void_p(_stream(stream))))
         return self.dx

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "sd_internal.h"
 
@@ -153,7 +154,7 @@ CUtensorMap out_map(void* c, int dt, int rows, int cols) {
 // two reach ~240 GB/s), so an operand tile is loaded in as few boxes as the
 // 128B swizzle allows.
 CUtensorMap kmajor_map(const void* p, int red, int rows) { return make_tmap_2d(p, false, red, rows, 64, 128); }
-CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_mn_atoms(p, mn, red); }
+CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_mn_atoms(p, mn, red, mn); }
 
 }  // namespace
 
@@ -235,11 +236,12 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
     return encode_tmap(base, f32, 2, dims, strides, box);
 }
 
-CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red) {
-    // view [red][mn] (mn contiguous) as (64 mn_in, red, mn / 64 atoms): one box
-    // = two 64-wide SW128 atoms of 64 reduction rows, atom-major in smem
+CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld) {
+    // view [red][mn] (mn contiguous, row pitch ld >= mn elements) as
+    // (64 mn_in, red, mn / 64 atoms): one box = two 64-wide SW128 atoms of 64
+    // reduction rows, atom-major in smem
     const cuuint64_t dims[3] = {64, red, mn / 64};
-    const cuuint64_t strides[2] = {mn * 2, 128};
+    const cuuint64_t strides[2] = {(ld ? ld : mn) * 2, 128};
     const cuuint32_t box[3] = {64, 64, 2};
     return encode_tmap(base, false, 3, dims, strides, box);
 }
@@ -504,6 +506,27 @@ GemmCall prep_layer_dx(const void* dy, const void* w, const sd_block_mask* mask,
     return prep_sdd(dy, w, true, mask, scale, dx, dx_dtype, m, k, n, nullptr, "layer backward dx");
 }
 
+// Rows [kb0, kb1) (mask-column blocks) of the layer's dW problem: the same
+// tiles, lists and reduction order as the full call, so each part is
+// bit-identical to those rows of the full dW (no cost order across parts).
+GemmCall prep_layer_dw_part(const GemmCall& full, const void* x, const sd_block_mask* mask, int m, int k, int n,
+                            int kb0, int kb1) {
+    const int kblk = mask->k_blk;
+    const int r0 = kb0 * kblk, rows = (kb1 - kb0) * kblk;
+    GemmCall g = full;
+    g.ta = make_tmap_mn_atoms(static_cast<const uint16_t*>(x) + r0, rows, m, k);
+    const bool f32 = full.args.flags & kFlagF32;
+    void* out = static_cast<char*>(full.args.out) + static_cast<size_t>(r0) * n * (f32 ? 4 : 2);
+    g.tout = out_map(out, f32 ? SD_DTYPE_F32 : SD_DTYPE_BF16, rows, n);
+    g.args.out = out;
+    g.args.rows_out = rows;
+    g.args.n_row_tiles = rows / kBM;
+    g.args.list_cnt = full.args.list_cnt + kb0;
+    g.args.list_idx = full.args.list_idx + static_cast<int64_t>(kb0) * full.args.list_stride;
+    g.args.row_order = nullptr;
+    return g;
+}
+
 // layer.hpp:159-160: dw (k x n) = s (x (.) m)^T dy over the mask's column lists —
 // the dsd problem (K_out = k rows, N, M_red = m) with x read MN-major in place.
 GemmCall prep_layer_dw(const void* x, const sd_block_mask* mask, const void* dy, float scale, void* dw,
@@ -551,6 +574,11 @@ struct sd_layer_plan {
     uint64_t threshold;
     int device;
     sd::GemmCall fwd, dw, dx, dense_fwd, dense_dw, dense_dx;
+    // dW split by mask-column blocks (data-parallel overlap of the all-reduce)
+    std::vector<sd::GemmCall> dw_part;
+    int dw_parts = 0;
+    const void* x = nullptr;
+    int m = 0, n = 0, k = 0;
     // (kept for ABI compatibility of the plan object; unused since the backward
     // runs as one fused launch)
     cudaStream_t aux = nullptr;
@@ -709,6 +737,8 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
+        tmp.x = x;
+        tmp.m = m, tmp.n = n, tmp.k = k;
         *out = new sd_layer_plan(tmp);
     });
 }
@@ -725,6 +755,27 @@ int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         launch_gemm(plan->dw, as_stream(stream));
+    });
+}
+
+int sd_layer_plan_backward_dw_part(sd_layer_plan* plan, int32_t part, int32_t nparts, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        const int cblocks = plan->mask.block_cols;
+        if (nparts < 1 || part < 0 || part >= nparts || nparts > cblocks)
+            fail(SD_ERANGE, "backward_dw_part: part " + str(part) + " of " + str(nparts) + " out of range for " +
+                                str(cblocks) + " mask columns");
+        if (plan->dw_parts != nparts) {
+            plan->dw_part.clear();
+            for (int i = 0; i < nparts; ++i) {
+                const int kb0 = static_cast<int>(static_cast<int64_t>(cblocks) * i / nparts);
+                const int kb1 = static_cast<int>(static_cast<int64_t>(cblocks) * (i + 1) / nparts);
+                plan->dw_part.push_back(prep_layer_dw_part(plan->dw, plan->x, &plan->mask, plan->m, plan->k,
+                                                           plan->n, kb0, kb1));
+            }
+            plan->dw_parts = nparts;
+        }
+        launch_gemm(plan->dw_part[part], as_stream(stream));
     });
 }
 

@@ -119,8 +119,8 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
 // 2D row-major tensor map: `inner` contiguous elements, `outer` rows, 128B swizzle.
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,
                          uint32_t box_inner, uint32_t box_outer);
-// bf16 [red][mn] operand (mn contiguous) as 3D (64, red, mn / 64): box = 128 mn
+// bf16 [red][mn] operand (mn contiguous, row pitch ld) as 3D (64, red, mn / 64): box = 128 mn
 // x 64 red in two atom-major 8 KB SW128 atoms; coordinates (0, red0, mn0 / 64).
-CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red);
+CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld);
 
 }  // namespace sd

@@ -159,3 +159,23 @@ def test_union_2cta_dsd_bitwise(sd, oracle, p):
     torch.cuda.synchronize()
     assert torch.equal(y2, plan.y)
     assert torch.equal(dw2, plan.dw)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+def test_dw_parts_equal_full_dw_bitwise(sd, oracle, nparts):
+    """sd_layer_plan_backward_dw_part: dW row slabs (mask-column blocks) for the
+    data-parallel all-reduce overlap reproduce backward_dw bit for bit."""
+    M, N, K, p = 2048, 1024, 1024, 0.5
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    plan = sd.LayerPlan(x, w, dy, p)
+    plan.forward(31)
+    plan.backward_dw()
+    torch.cuda.synchronize()
+    full = plan.dw.clone()
+    plan.dw.fill_(float("nan"))
+    slabs = [plan.backward_dw_part(i, nparts) for i in range(nparts)]
+    torch.cuda.synchronize()
+    assert sum(s.shape[0] for s in slabs) == K
+    assert torch.equal(plan.dw, full)
+    with pytest.raises(IndexError):
+        plan.backward_dw_part(nparts, nparts)
