@@ -52,6 +52,7 @@ struct PlanArgs {
     uint64_t seed_mix;   // mix64(seed): counter_hash = mix64(mix64(seed_mix ^ r) ^ c)
     uint64_t threshold;  // ceil(p * 2^53)
     int nb_words, nb_rows, nb_cols;
+    int inline_order;  // one extra block computes counts, keep_count and the orders itself
 };
 
 __device__ __forceinline__ bool keep_bit(const PlanArgs& a, int r, int c) {
@@ -107,6 +108,14 @@ __device__ void scan_desc(int* bins, int n, int* warp_tot) {
 }
 
 // Counting sort of `count` (values in [0, max_val]) into a descending order.
+// `count` is global memory written by other blocks of this grid (read through
+// L2), or this block's shared memory.
+template <bool SMEM>
+__device__ __forceinline__ int read_count(const int32_t* count, int i) {
+    if constexpr (SMEM) return count[i];
+    else return __ldcg(count + i);
+}
+template <bool SMEM = false>
 __device__ void order_by_count(const int32_t* count, int n, int max_val, int32_t* order, int* bins,
                                int* warp_tot) {
     if (max_val + 1 > kMaxOrderBins) {
@@ -116,11 +125,11 @@ __device__ void order_by_count(const int32_t* count, int n, int max_val, int32_t
     const int nb = max_val + 1;
     for (int i = threadIdx.x; i < nb; i += kThreads) bins[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&bins[__ldcg(count + i)], 1);
+    for (int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&bins[read_count<SMEM>(count, i)], 1);
     __syncthreads();
     scan_desc(bins, nb, warp_tot);
     for (int i = threadIdx.x; i < n; i += kThreads) {
-        const int pos = atomicAdd(&bins[__ldcg(count + i)], 1);
+        const int pos = atomicAdd(&bins[read_count<SMEM>(count, i)], 1);
         order[pos] = i;
     }
     __syncthreads();
@@ -135,15 +144,63 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     int blk = blockIdx.x;
-    // the consumer GEMM may start its prologue now; its griddepcontrol.wait
-    // still orders all of its reads after this grid completes
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(a.trace_id & 255) * 4 + 0], gtimer_m());
 #endif
     // our own inputs (mask words in compact mode) come from earlier work
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 1], gtimer_m());  // last block past wait
+#endif
 
+    if (a.inline_order && blk == a.nb_words + a.nb_rows + a.nb_cols) {
+        // ---- counts, keep_count and cost orders, recomputed by this block alone
+        // from (seed, r, c) (or the given words) while the other blocks write the
+        // words and lists: no grid-wide ticket and serial last block on the
+        // critical path (that phase cost 4-8 us per mask, ~3% of a 4096^3 step).
+        int* rc = dyn_smem;
+        int* cc = rc + R;
+        int* bins = cc + C;
+        for (int i = threadIdx.x; i < R + C; i += kThreads) rc[i] = 0;
+        __syncthreads();
+        for (int r = wid; r < R; r += kThreads / 32) {
+            const uint64_t hr = mix64(a.seed_mix ^ static_cast<uint64_t>(r + a.m.row_block_offset));
+            int cnt = 0;
+            for (int c0 = 0; c0 < C; c0 += 32) {
+                const int c = c0 + lane;
+                bool k = false;
+                if (c < C) {
+                    if (a.from_words) {
+                        const int64_t b = static_cast<int64_t>(r) * C + c;
+                        k = (a.m.words[b >> 6] >> (b & 63)) & 1ull;
+                    } else {
+                        k = (mix64(hr ^ static_cast<uint64_t>(c)) >> 11) >= a.threshold;
+                    }
+                }
+                cnt += __popc(__ballot_sync(0xffffffffu, k));
+                if (k) atomicAdd(&cc[c], 1);
+            }
+            if (lane == 0) rc[r] = cnt;
+        }
+        __syncthreads();
+        unsigned long long kc = 0;
+        for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(rc[r]);
+        for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+        if (lane == 0) keep_part[wid] = kc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long sum = 0;
+            for (int i = 0; i < kThreads / 32; ++i) sum += keep_part[i];
+            *a.m.keep_count = static_cast<int64_t>(sum);
+        }
+        order_by_count<true>(rc, R, C, a.m.row_order, bins, warp_tot);
+        order_by_count<true>(cc, C, R, a.m.col_order, bins, warp_tot);
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef SD_TRACE
+        if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
+#endif
+        return;
+    }
     if (blk < a.nb_words) {
         // ---- words: one warp per 64-bit word, two bits per lane, ballot-packed
         const int64_t total = static_cast<int64_t>(R) * C;
@@ -213,6 +270,19 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         __syncthreads();
     }
 
+    // Only now let the consumer GEMM launch: its 1-CTA-per-SM blocks (227 KB of
+    // shared memory) would otherwise take the SMs freed by the previous GEMM's
+    // tail and wait there for this grid, starving our own blocks (measured: the
+    // mask took ~15 us after the previous backward instead of ~6). Its
+    // griddepcontrol.wait still orders all of its reads after this grid.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (a.inline_order) {
+#ifdef SD_TRACE
+        if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
+#endif
+        return;
+    }
+
     // ---- last block: keep_count and cost orders
     __threadfence();
     __syncthreads();
@@ -223,6 +293,9 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     __syncthreads();
     if (!is_last) return;
     __threadfence();
+#ifdef SD_TRACE
+    if (threadIdx.x == 0) g_sd_timeline[(a.trace_id & 255) * 4 + 3] = gtimer_m();  // ordering phase starts
+#endif
 
     unsigned long long kc = 0;
     for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(__ldcg(a.m.row_cnt + r));
@@ -289,10 +362,16 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     a.nb_words = from_words ? 0 : static_cast<int>((nwords + kThreads / 32 - 1) / (kThreads / 32));
     a.nb_rows = (m.block_rows + kThreads / 32 - 1) / (kThreads / 32);
     a.nb_cols = m.block_cols;
-    const int grid = a.nb_words + a.nb_rows + a.nb_cols;
+    // counts + orders in one extra block when the grid is small enough for one
+    // block to re-evaluate every bit cheaply (every BASELINE config up to
+    // 512 x 64; cfg5's 4096 x 64 single-GPU shard uses the ticketed last block)
+    const int64_t nbits = static_cast<int64_t>(m.block_rows) * m.block_cols;
+    a.inline_order = (nbits <= 32768 && m.block_rows <= 4096 && m.block_cols <= 4096) ? 1 : 0;
+    const int grid = a.nb_words + a.nb_rows + a.nb_cols + a.inline_order;
     const int bins = std::min(std::max(m.block_rows, m.block_cols) + 1, kMaxOrderBins);
     const int chunks = (m.block_rows + 31) / 32;
-    const size_t smem = static_cast<size_t>(std::max(bins, chunks)) * sizeof(int);
+    const int inline_ints = a.inline_order ? m.block_rows + m.block_cols + bins : 0;
+    const size_t smem = static_cast<size_t>(std::max({bins, chunks, inline_ints})) * sizeof(int);
     if (smem > 48 * 1024) {
         static bool raised = false;
         if (!raised) {
@@ -344,7 +423,8 @@ extern "C" SD_API int sd_mask_timeline_read(unsigned long long* host) {
     if (cudaMemcpyFromSymbol(host, sd::g_sd_timeline, sizeof(unsigned long long) * 256 * 4) != cudaSuccess)
         return SD_ERUNTIME;
     static unsigned long long init[256 * 4];
-    for (int i = 0; i < 256; ++i) init[4 * i] = init[4 * i + 1] = ~0ull, init[4 * i + 2] = init[4 * i + 3] = 0;
+    // {first block start (min), last block past griddepcontrol.wait (max), end (max), ordering start}
+    for (int i = 0; i < 256; ++i) init[4 * i] = ~0ull, init[4 * i + 1] = init[4 * i + 2] = init[4 * i + 3] = 0;
     cudaMemcpyToSymbol(sd::g_sd_timeline, init, sizeof init);
     return SD_OK;
 }

@@ -1,6 +1,6 @@
 """Device timeline of one SparseDrop layer step (dev tool; needs `make trace`).
 
-  SPARSEDROP_B200_LIB=paper_2411_01238_b200/lib/libsparsedrop_b200_trace.so python tools/timeline.py [SIZE] [P]
+  SPARSEDROP_B200_LIB=paper_2411_01238_b200/lib/libsparsedrop_b200_trace.so python tools/timeline.py [SIZE] [P] [STEPS]
 Prints, per launch of the step, the first CTA's start, when it passed
 griddepcontrol.wait (PDL), and the last CTA's end (globaltimer, ns)."""
 import ctypes
@@ -20,6 +20,7 @@ lib.sd_timeline_read.argtypes = [ctypes.c_void_p]
 lib.sd_mask_timeline_read.argtypes = [ctypes.c_void_p]
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 P = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
+BACK_TO_BACK = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # steps per timed burst (bench.py runs them back to back)
 x = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 w = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 dy = torch.randn(S, S, device="cuda").to(torch.bfloat16)
@@ -35,8 +36,9 @@ for it in range(4):
     l0 = sd.launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    plan.forward(it)
-    plan.backward()
+    for rep in range(BACK_TO_BACK):
+        plan.forward(it * 8 + rep)
+        plan.backward()
     b.record()
     torch.cuda.synchronize()
     l1 = sd.launch_count()
@@ -54,7 +56,11 @@ for it in range(4):
     print(f"-- step {it}: event time {a.elapsed_time(b) * 1e3:.1f} us; device span {(max(r[4] for r in rows) - t0) / 1e3:.1f} us")
     prev_end = None
     for st, name, lid, wt, en in rows:
-        wait = "" if wt == 0xFFFFFFFFFFFFFFFF or name == "mask" else f" past-wait {(wt - t0) / 1e3:7.1f}"
+        if name == "mask":
+            lw, od = int(mk[4 * (lid & 255) + 1]), int(mk[4 * (lid & 255) + 3])
+            wait = (f" last-past-wait {(lw - t0) / 1e3:7.1f}" if lw else "") + (f" order {(od - t0) / 1e3:7.1f}" if od else "")
+        else:
+            wait = "" if wt == 0xFFFFFFFFFFFFFFFF else f" past-wait {(wt - t0) / 1e3:7.1f}"
         gap = "" if prev_end is None else f" (gap from prev end {(st - prev_end) / 1e3:+.1f})"
         print(f"   {name:5s} #{lid}: start {(st - t0) / 1e3:7.1f}{wait} end {(en - t0) / 1e3:7.1f}  dur {(en - st) / 1e3:6.1f} us{gap}")
         prev_end = en
