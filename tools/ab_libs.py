@@ -18,9 +18,22 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_01238_b200._capi import SdBlockMask  # noqa: E402
 
 
+_loaded = set()
+
+
 def load(spec):
     path, _, tune = spec.partition(":")
-    lib = ctypes.CDLL(os.path.abspath(path), mode=ctypes.RTLD_LOCAL)
+    path = os.path.abspath(path)
+    if path in _loaded:
+        # dlopen of the same path returns the same instance (one tuning state):
+        # A/B two tunings of one build through a private copy
+        import shutil
+        import tempfile
+        copy = os.path.join(tempfile.mkdtemp(), os.path.basename(path))
+        shutil.copy(path, copy)
+        path = copy
+    _loaded.add(path)
+    lib = ctypes.CDLL(path, mode=ctypes.RTLD_LOCAL)
     lib.sd_mask_workspace_bytes.restype = ctypes.c_size_t
     lib.sd_set_tuning(int(tune or 0))
     return lib
