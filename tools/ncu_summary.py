@@ -16,11 +16,14 @@ KEYS = [
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
-    ("lts__t_bytes.sum", "l2_bytes"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_to_sm_read_sectors"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_pct"),
-    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_pct_elapsed"),
-    ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", "tc_bf16_ops_pct"),
-    ("sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active", "hmma_inst_pct_active"),
+    # tcgen05 (UTC*) tensor pipe: the metrics that see sm_100 MMAs. The legacy
+    # HMMA-pipe counters (sm__pipe_tensor_cycles_active_realtime,
+    # sm__inst_executed_pipe_tensor_subpipe_hmma) stay at ~0 for tcgen05 kernels.
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tc_pipe_pct_active"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "tc_pipe_pct_elapsed"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tmem_pct_active"),
     ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem_tc_pct"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_pct"),
     ("launch__registers_per_thread", "regs"),
