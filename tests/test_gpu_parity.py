@@ -67,6 +67,9 @@ def words_np(mask):
 MASK_GEOMS = [
     (1024, 1024, 0), (4096, 4096, 0), (65536, 768, 0x238275BC38FCBE91), (65536, 3072, 5),
     (65536, 8192, 0), (8192, 8192, 0), (128 * 37, 128 * 19, 3), (128, 128, 1), (128 * 5, 128 * 70, 2),
+    # > 32768 blocks or > 4096 rows: counts and orders from the ticketed last
+    # block instead of the inline order block (sd_mask.cu)
+    (524288, 8192, 0), (128 * 4100, 256, 7),
 ]
 
 
