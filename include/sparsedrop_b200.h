@@ -228,7 +228,9 @@ SD_API uint64_t sd_launch_count(void);
  * 8 backward as two launches instead of one fused launch,
  * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA
  *    (cta_group::2) kernel,
- * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles. */
+ * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles
+ *    (default: 128x512 for dsd-only launches with a keep hint >= 0.2).
+ * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 
 #ifdef __cplusplus
