@@ -10,6 +10,9 @@ cfg5  one GPU's row shard of M=524288, K=N=8192 (the G=1 point), p=0.1/0.5
 Timing: CUDA events per step, L2 flushed between steps, 0.3 s sustained
 pre-roll per configuration (steady power-capped state); dense-equivalent and
 executed TFLOP/s, speed-up vs our dense tcgen05 path on the same buffers.
+Beside each: the reference CPU layer fwd+bwd (oracle/_ref, all host threads,
+float) on a row slab of the same problem, extrapolated linearly in M (every
+GEMM of the layer, dW included, is linear in M) — SURVEY §8(d).
 """
 import argparse
 import json
@@ -58,7 +61,34 @@ def timed(step, steps, preroll_s=0.3):
     return tot / steps
 
 
-def layer_cfg(name, M, N, K, ps, steps):
+def cpu_reference(M, N, K, p, slab_rows):
+    """The reference's layer fwd+bwd (mask generation included) on the first
+    `slab_rows` rows, timed with all host threads; ms extrapolated to M rows."""
+    import os
+
+    import numpy as np
+
+    from oracle.oracle import REF_LIB, Oracle, Reference
+
+    if not REF_LIB.exists():
+        return None
+    o, ref = Oracle(), Reference()
+    # the reference parallelises the forward and dX over 128-row tile rows:
+    # give every host thread one (SURVEY §8d: 16 M-blocks on a 16-core host)
+    threads = os.cpu_count() or 1
+    rows = min(M, max(slab_rows, 128 * threads))
+    x = o.random_matrix(rows, K, 1).astype(np.float32)
+    w = o.random_matrix(K, N, 2).astype(np.float32)
+    dy = o.random_matrix(rows, N, 3).astype(np.float32)
+    t0 = time.perf_counter()
+    ref.layer_fwd_bwd(x, w, dy, p, 128, 128, 128, seed=0, step_seed=0, layer_index=0, threads=threads,
+                      dtype=np.float32)
+    t = time.perf_counter() - t0
+    return {"slab_rows": rows, "slab_seconds": t, "threads": threads, "kind": "reference",
+            "ms_per_step_extrapolated": t * 1e3 * M / rows}
+
+
+def layer_cfg(name, M, N, K, ps, steps, slab_rows=512):
     x, w, dy = synth(M, K), synth(K, N), synth(M, N)
     out = []
     dense_ms = None
@@ -69,11 +99,15 @@ def layer_cfg(name, M, N, K, ps, steps):
         keep = plan.mask.keep_count() / plan.mask.total_blocks()
         if dense_ms is None:
             dense_ms = timed(lambda i: (plan.dense_forward(), plan.dense_backward()), steps)
+        cpu = cpu_reference(M, N, K, p, slab_rows)
+        if cpu:
+            cpu["dense_equiv_tflops"] = flops / (cpu["ms_per_step_extrapolated"] * 1e-3) / 1e12
+            cpu["gpu_speedup"] = cpu["ms_per_step_extrapolated"] / ms
         out.append({"config": name, "M": M, "N": N, "K": K, "p": p, "keep": keep, "ms_per_step": ms,
                     "dense_ms_per_step": dense_ms, "speedup_vs_dense": dense_ms / ms,
                     "dense_equiv_tflops": flops / (ms * 1e-3) / 1e12,
                     "executed_tflops": keep * flops / (ms * 1e-3) / 1e12,
-                    "dense_tflops": flops / (dense_ms * 1e-3) / 1e12})
+                    "dense_tflops": flops / (dense_ms * 1e-3) / 1e12, "cpu_reference": cpu})
         print(json.dumps(out[-1]), flush=True)
         del plan
     del x, w, dy
@@ -95,11 +129,19 @@ def mlp_cfg(ps, steps):
         k1 = mlp.fc1.mask.keep_count() / mlp.fc1.mask.total_blocks()
         k2 = mlp.fc2.mask.keep_count() / mlp.fc2.mask.total_blocks()
         keep = (k1 + k2) / 2
+        c1, c2 = cpu_reference(M, H, D, p, 1024), cpu_reference(M, D, H, p, 1024)
+        cpu = None
+        if c1 and c2:
+            cms = c1["ms_per_step_extrapolated"] + c2["ms_per_step_extrapolated"]
+            cpu = {"kind": "reference", "threads": c1["threads"], "slab_rows": c1["slab_rows"],
+                   "ms_per_step_extrapolated": cms, "dense_equiv_tflops": flops / (cms * 1e-3) / 1e12,
+                   "gpu_speedup": cms / ms, "note": "fc1 + fc2 layer fwd+bwd (the reference has no GELU)"}
         out.append({"config": "cfg3_vit_b_mlp", "tokens": M, "dims": [D, H, D], "p": p, "keep_fc1": k1,
                     "keep_fc2": k2, "ms_per_step": ms, "dense_ms_per_step": dense_ms,
                     "speedup_vs_dense": dense_ms / ms, "dense_equiv_tflops": flops / (ms * 1e-3) / 1e12,
                     "executed_tflops": keep * flops / (ms * 1e-3) / 1e12,
-                    "note": "GELU/GELU' are torch elementwise ops inside the timed step"})
+                    "note": "GELU / GELU' are this library's single-pass bf16 kernels inside the timed step",
+                    "cpu_reference": cpu})
         print(json.dumps(out[-1]), flush=True)
         del mlp
     del x, w1, w2, dy
@@ -113,7 +155,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     res = []
-    res += layer_cfg("cfg1", 1024, 1024, 1024, [0.5], 20)
+    res += layer_cfg("cfg1", 1024, 1024, 1024, [0.5], 20, slab_rows=1024)
     res += mlp_cfg([0.1, 0.5], 5 if args.quick else 10)
     res += layer_cfg("cfg4", 65536, 8192, 8192, [0.1, 0.3, 0.5], 3 if args.quick else 5)
     if not args.quick:
