@@ -743,11 +743,18 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
     });
 }
 
+// p = 0 keeps every block: the step is the dense layer, and the dense kernels
+// (2-CTA when the shape allows) give bit-identical outputs — every element is
+// reduced over the same 16-deep MMA steps in the same order
+// (tests/test_gpu_kernel_modes.py::test_p0_plan_equals_sparse_kernels). The
+// (all-kept) mask is still generated: the caller's BlockMask stays valid.
+static bool plan_dense(const sd_layer_plan* plan) { return plan->p == 0.0 && !(tuning() & kTuneNarrow); }
+
 int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, as_stream(stream));
-        launch_gemm(plan->fwd, as_stream(stream));
+        launch_gemm(plan_dense(plan) ? plan->dense_fwd : plan->fwd, as_stream(stream));
     });
 }
 
@@ -789,7 +796,8 @@ int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
 int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        fused_backward(plan->dx, plan->dw, as_stream(stream));
+        if (plan_dense(plan)) fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream));
+        else fused_backward(plan->dx, plan->dw, as_stream(stream));
     });
 }
 

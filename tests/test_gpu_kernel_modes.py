@@ -179,3 +179,29 @@ def test_dw_parts_equal_full_dw_bitwise(sd, oracle, nparts):
     assert torch.equal(plan.dw, full)
     with pytest.raises(IndexError):
         plan.backward_dw_part(nparts, nparts)
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 1024), (2048, 768, 3072), (512, 1536, 640)])
+def test_p0_plan_equals_sparse_kernels(sd, oracle, M, N, K):
+    """A p = 0 layer plan runs the dense kernels (nothing to skip); its outputs
+    equal the masked kernels' bit for bit (generic C-ABI dsd / sdd entries)."""
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    plan = sd.LayerPlan(x, w, dy, 0.0)
+    plan.forward(5)
+    plan.backward()
+    torch.cuda.synchronize()
+    m = plan.mask
+    assert m.keep_count() == m.total_blocks()
+    lib = sd.load_library()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    y = torch.empty_like(plan.y)
+    dx = torch.empty_like(plan.dx)
+    dw = torch.empty_like(plan.dw)
+    sd.api.check(lib.sd_linear_forward(x.data_ptr(), m.cptr(), w.data_ptr(), 1.0, y.data_ptr(), 1, M, N, K, st))
+    sd.api.check(lib.sd_linear_backward_dx(dy.data_ptr(), w.data_ptr(), m.cptr(), 1.0, dx.data_ptr(), 1, M, N, K, st))
+    sd.api.check(lib.sd_linear_backward_dw(x.data_ptr(), m.cptr(), dy.data_ptr(), 1.0, dw.data_ptr(), 0, M, N, K, st))
+    torch.cuda.synchronize()
+    assert torch.equal(plan.y, y)
+    assert torch.equal(plan.dx, dx)
+    if not torch.equal(plan.dw, dw):  # split-K (small dW outputs) reduces in arrival order
+        assert torch.allclose(plan.dw, dw, rtol=1e-5, atol=1e-5 * float(dw.abs().max()))
