@@ -205,3 +205,20 @@ def test_p0_plan_equals_sparse_kernels(sd, oracle, M, N, K):
     assert torch.equal(plan.dx, dx)
     if not torch.equal(plan.dw, dw):  # split-K (small dW outputs) reduces in arrival order
         assert torch.allclose(plan.dw, dw, rtol=1e-5, atol=1e-5 * float(dw.abs().max()))
+
+
+def test_gelu_table_equals_direct_all_bf16(sd):
+    """sd_gelu_forward on large activations reads a 64 K-entry table built with
+    the direct kernel's math: every bf16 bit pattern (NaN/Inf included) must map
+    to the same output bits as the direct evaluation (used below 512 K elements)."""
+    from paper_2411_01238_b200.mlp import gelu
+
+    pats = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.int16).view(torch.bfloat16)
+    big = pats.repeat(16)                         # 1 M elements: table path
+    small = pats[: 65536 // 2].clone(), pats[65536 // 2:].clone()  # 32 K each: direct path
+    out_big = gelu(big)
+    out_small = torch.cat([gelu(small[0]), gelu(small[1])])
+    torch.cuda.synchronize()
+    ref = out_small.view(torch.int16)
+    assert torch.equal(out_big.view(torch.int16)[:65536], ref)
+    assert torch.equal(out_big.view(torch.int16).view(16, 65536), ref.expand(16, 65536))
