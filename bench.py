@@ -430,13 +430,13 @@ def main():
     # ---- dense baseline (same kernel, no mask) and cuBLAS for context
     ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup)
     # the same dense step on the 1-CTA tile machinery the masked GEMMs use
-    # (tuning 1|16: no 2-CTA kernel) — the like-for-like (1-p) reference
+    # (tuning 16: no 2-CTA kernel) — the like-for-like (1-p) reference
     _lib_t = sd.load_library()
-    _lib_t.sd_set_tuning(1 | 16)
+    _lib_t.sd_set_tuning(16)
     try:
         ms_dense_1cta = time_steps(dense_step_fn(), args.steps, args.warmup)
     finally:
-        _lib_t.sd_set_tuning(1)
+        _lib_t.sd_set_tuning(0)
     ms_torch = time_steps(torch_step, args.steps, args.warmup)
 
     # ---- per-kernel durations at the headline p (roofline): each kernel run

@@ -222,8 +222,8 @@ SD_API uint64_t sd_flops_effective(int64_t n, int64_t k, int32_t m_blk, int32_t 
  * native path ran; see bench.py "gpu_launches"). */
 SD_API uint64_t sd_launch_count(void);
 
-/* Scheduler tuning switches for A/B measurements (default 1):
- * 1 no tail halving (half-width units for the last wave; measured a net loss),
+/* Scheduler tuning switches for A/B measurements (default 0):
+ * 1 no tail halving (half-width units for about the last half wave of narrow launches),
  * 2 no split-K, 4 no heaviest-first row order,
  * 8 backward as two launches instead of one fused launch,
  * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA

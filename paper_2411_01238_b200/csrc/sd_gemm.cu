@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // SD_TUNING (environment) overrides the default for whole-process A/B runs.
 static int initial_tuning() {
     const char* e = std::getenv("SD_TUNING");
-    return e ? std::atoi(e) : kTuneNoTailHalving;
+    return e ? std::atoi(e) : 0;
 }
 static int g_tuning = initial_tuning();
 int tuning() { return g_tuning; }
@@ -888,7 +888,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
         order[1] = 0;
     }
     // tail halving on the problem handed out last, when the launch is only a
-    // few waves deep: its lightest ~2 waves of units become half-width
+    // few waves deep: its lightest ~half wave of units become half-width
     {
         int total_units = 0;
         for (int i = 0; i < n; ++i) total_units += gemm_units(pa[i]);
@@ -896,7 +896,11 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
         const bool sdd = last.flags & kFlagSDD;
         if (!wide && !(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units < 12 * sms &&
             (!sdd || last.out_col_blk == 128)) {
-            const int T = (sms + last.n_col_units - 1) / last.n_col_units;
+            // about half a wave of half-width units: measured -2.5% on the 4096^3
+            // fused backward at p = 0.5 and -5% on dX at p = 0.1; two waves' worth
+            // cost more operand traffic than the shorter tail saves
+            // (profiles/r01_tail_halving_ab.txt)
+            const int T = (sms + 4 * last.n_col_units - 1) / (4 * last.n_col_units);
             last.tail_rows = std::min(T, last.n_row_tiles);
         }
     }

@@ -63,7 +63,7 @@ def test_layer_wide_equals_narrow_bitwise(sd, oracle, M, N, K, p, fused):
         lib.sd_set_tuning(WIDE)
         got = _layer_outputs(sd, x, w, dy, p, 21, fused)
     finally:
-        lib.sd_set_tuning(1)
+        lib.sd_set_tuning(0)
     for name, a, b in zip(("y", "dx", "dw"), ref, got):
         if name == "dw" and not torch.equal(a, b):
             # split-K dW (small outputs) reduce-adds partials in arrival order:
@@ -89,7 +89,7 @@ def test_generic_sdd_and_dsd_wide_equals_narrow(sd, oracle, n_blk):
                           sd.sdd_matmul(a, b, m_sdd, 1.5, out_dtype=torch.bfloat16))
         torch.cuda.synchronize()
     finally:
-        lib.sd_set_tuning(1)
+        lib.sd_set_tuning(0)
     for u, v in zip(outs[NARROW], outs[WIDE]):
         assert torch.equal(u, v)
 
@@ -105,7 +105,7 @@ def test_wide_forward_matches_oracle(sd, oracle):
         y = sd.dsd_matmul(x, m, w, s, out_dtype=torch.float32)
         torch.cuda.synchronize()
     finally:
-        lib.sd_set_tuning(1)
+        lib.sd_set_tuning(0)
     words = np.array(m.words(), dtype=np.uint64)
     xn, wn = x.double().cpu().numpy(), w.double().cpu().numpy()
     ref = oracle.dsd_matmul(xn, words, wn, 128, 128, 128, s)

@@ -216,7 +216,7 @@ def test_dense_2cta_equals_1cta_bitwise(sd, oracle, layout):
                 outs[(tune, code)] = c
         torch.cuda.synchronize()
     finally:
-        lib.sd_set_tuning(1)
+        lib.sd_set_tuning(0)
     for code in (0, 1):
         assert torch.equal(outs[(1 | 16, code)], outs[(1, code)])
 

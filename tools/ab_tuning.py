@@ -55,4 +55,4 @@ for v in variants:
     med = {k: sorted(a)[len(a) // 2] for k, a in res[v].items()}
     print(f"S={S} p={P} tuning={v}: step {med['step']:.1f} us (fwd {med['fwd']:.1f}, bwd {med['bwd']:.1f}; "
           f"dw {med['dw']:.1f}, dx {med['dx']:.1f}), dense {med['dense']:.1f} us", flush=True)
-lib.sd_set_tuning(1)
+lib.sd_set_tuning(0)

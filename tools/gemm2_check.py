@@ -57,4 +57,4 @@ for S in sizes:
             print(f"S={S} {name} tuning={tune}: rel_err {err:.2e}  {us:8.1f} us  {tf:7.1f} TF/s", flush=True)
         d = (res[17] - res[1]).abs().max().item()
         print(f"   max |1cta - 2cta| = {d:.3e}", flush=True)
-lib.sd_set_tuning(1)
+lib.sd_set_tuning(0)

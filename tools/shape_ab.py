@@ -36,7 +36,7 @@ for r in range(rounds):
             e1.record()
             torch.cuda.synchronize()
             res[t][k].append(e0.elapsed_time(e1) * 1e3)
-lib.sd_set_tuning(1)
+lib.sd_set_tuning(0)
 for t in tunings:
     med = {k: sorted(v)[len(v) // 2] for k, v in res[t].items()}
     print(f"M={M} N={N} K={K} p={P} tuning={t}: fwd {med['fwd']:.1f} us  bwd {med['bwd']:.1f} us", flush=True)

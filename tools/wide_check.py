@@ -62,5 +62,5 @@ for (M, N, K, p) in shapes:
             torch.cuda.synchronize()
             t = [ev[j].elapsed_time(ev[j + 1]) / n * 1e3 for j in range(4)]
             print(f"   tuning={tune}: fwd {t[0]:.1f} us  bwd {t[1]:.1f} us  (dw {t[2]:.1f}, dx {t[3]:.1f})", flush=True)
-lib.sd_set_tuning(1)
+lib.sd_set_tuning(0)
 print("ALL EQUAL" if ok else "MISMATCH")
