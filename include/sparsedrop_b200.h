@@ -66,7 +66,8 @@ typedef struct sd_block_mask {
     int32_t* col_idx;     /* C*R: kept_blocks_in_row(transpose_mask(mask), c)     */
     int32_t* row_order;   /* R: block rows by kept count, descending (scheduling)  */
     int32_t* col_order;   /* C: block columns by kept count, descending           */
-    uint32_t* ticket;     /* 1: internal completion counter (keep zero)           */
+    uint32_t* ticket;     /* internal counters (keep zero; sd_mask_bind reserves 256 B:
+                             [0] completion ticket, [1] reader release count) */
 } sd_block_mask;
 
 SD_API int sd_abi_version(void);
@@ -229,7 +230,13 @@ SD_API uint64_t sd_launch_count(void);
  * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA
  *    (cta_group::2) kernel,
  * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles
- *    (default: 128x512 for dsd-only launches with a keep hint >= 0.2).
+ *    (default: 128x512 for dsd-only launches with a keep hint >= 0.2),
+ * 128 a layer plan's backward waits for its forward grid (default: the first
+ *    backward launch right after the plan's forward starts on the SMs the
+ *    forward's last wave frees; it reads nothing the forward writes),
+ * 256 mask generation waits for the whole preceding grid (default, for a
+ *    workspace bound by sd_mask_bind: only for the GEMM CTAs still reading its
+ *    previous lists, which release it when their last list read is done).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 

@@ -77,6 +77,7 @@ PROTOTYPES = {
     "sd_layer_plan_backward_dw": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_backward_dx": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_backward_dw_part": (ctypes.c_int, [_P, _I, _I, _P]),
+    "sd_dev_mask_counter_waits": (ctypes.c_uint64, []),
     "sd_dev_dsd_pairs": (ctypes.c_int, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _I, ctypes.c_float, _P]),
     "sd_layer_plan_dense_forward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),

@@ -198,6 +198,99 @@ unsigned int* sched_slot() {
     return slots[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
 }
 
+// ---------------------------------------------------------------- reader tracking
+// One entry per workspace bound by sd_mask_bind: its byte range, its release
+// counter (the second word of the 256-byte ticket slot) and the reader CTAs
+// launched since the last generation into it. The counter protocol is only
+// used when every such reader ran on the generation's own stream (so each of
+// them is either complete or resident when the generation starts: no reader
+// can wait for SMs held by the generation's spinning blocks) and outside
+// stream capture; any doubt -> the generation falls back to
+// griddepcontrol.wait, which covers every earlier grid of the stream.
+namespace {
+struct ReaderEntry {
+    uintptr_t base, end;
+    unsigned int* rel;
+    uint32_t pending;
+    cudaStream_t stream;
+    bool mixed;
+};
+std::mutex g_reader_mu;
+std::vector<ReaderEntry> g_readers;
+
+ReaderEntry* find_reader_entry(uintptr_t p) {
+    for (auto& e : g_readers)
+        if (p >= e.base && p < e.end) return &e;
+    return nullptr;
+}
+}  // namespace
+
+void mask_register_workspace(void* ws, size_t bytes, unsigned int* rel) {
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    const uintptr_t b = reinterpret_cast<uintptr_t>(ws), e = b + bytes;
+    for (size_t i = 0; i < g_readers.size();) {
+        if (g_readers[i].base < e && b < g_readers[i].end) {
+            g_readers[i] = g_readers.back();
+            g_readers.pop_back();
+        } else {
+            ++i;
+        }
+    }
+    if (g_readers.size() >= 4096) g_readers.erase(g_readers.begin());  // untracked from now on: safe
+    g_readers.push_back({b, e, rel, 0u, nullptr, false});
+}
+
+// Exact match on the counter address: only a struct filled by sd_mask_bind
+// (whose ticket slot is 256 bytes) gets a counter; the library never writes
+// the counter of a range it merely overlaps.
+unsigned int* mask_release_counter(const sd_block_mask* m) {
+    if (!m || !m->ticket) return nullptr;
+    unsigned int* rel = m->ticket + 1;
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    for (const auto& e : g_readers)
+        if (e.rel == rel) return rel;
+    return nullptr;
+}
+
+void mask_note_readers(unsigned int* rel, int ctas, cudaStream_t s) {
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    for (auto& e : g_readers) {
+        if (e.rel != rel) continue;
+        if (e.pending > 0 && e.stream != s) e.mixed = true;
+        e.stream = s;
+        e.pending += static_cast<uint32_t>(ctas);
+        return;
+    }
+}
+
+void mask_note_untracked(const void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    if (ReaderEntry* e = find_reader_entry(reinterpret_cast<uintptr_t>(p))) e->mixed = true;
+}
+
+std::atomic<uint64_t> g_counter_waits{0};
+void note_counter_wait() { g_counter_waits.fetch_add(1, std::memory_order_relaxed); }
+
+bool mask_take_release(unsigned int* rel, cudaStream_t s, uint32_t* target) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        cap = cudaStreamCaptureStatusActive;
+    }
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    for (auto& e : g_readers) {
+        if (e.rel != rel) continue;
+        const bool ok = !e.mixed && e.pending > 0 && e.stream == s && cap == cudaStreamCaptureStatusNone;
+        *target = e.pending;
+        e.pending = 0;
+        e.mixed = false;
+        e.stream = s;
+        return ok;
+    }
+    return false;
+}
+
 static CUtensorMap encode_tmap(const void* base, bool f32, cuuint32_t rank, const cuuint64_t* dims,
                                const cuuint64_t* strides, const cuuint32_t* box) {
     std::call_once(g_encode_once, [] {
@@ -358,6 +451,8 @@ int sd_mask_bind(sd_block_mask* m, void* ws, int32_t R, int32_t C, int32_t m_blk
         m->row_order = reinterpret_cast<int32_t*>(p);
         p += align256(4 * static_cast<size_t>(R));
         m->col_order = reinterpret_cast<int32_t*>(p);
+        // the ticket slot is 256 bytes: word 1 is the reader release counter
+        mask_register_workspace(ws, sd_mask_workspace_bytes(R, C), m->ticket + 1);
     });
 }
 
@@ -462,6 +557,7 @@ GemmCall prep_dsd_forward(const void* a, const sd_block_mask* mask, const void* 
     g.args.flags = flags_of(false, true, false, c_dtype);
     g.args.list_cnt = mask->row_cnt;
     g.args.list_idx = mask->row_idx;
+    g.release = mask_release_counter(mask);
     g.args.list_stride = mask->block_cols;
     g.args.red_blk = mask->k_blk;
     g.args.out_row_blk = mask->m_blk;
@@ -491,6 +587,7 @@ GemmCall prep_sdd(const void* a, const void* b, bool b_kmajor, const sd_block_ma
     g.args.words = mask->words;
     g.args.list_cnt = mask->row_cnt;
     g.args.list_idx = mask->row_idx;
+    g.release = mask_release_counter(mask);
     g.args.list_stride = mask->block_cols;
     g.args.mask_cols = mask->block_cols;
     g.args.out_col_blk = mask->k_blk;
@@ -547,6 +644,7 @@ GemmCall prep_layer_dw(const void* x, const sd_block_mask* mask, const void* dy,
     g.args.flags = flags_of(true, true, false, dw_dtype);
     g.args.list_cnt = mask->col_cnt;
     g.args.list_idx = mask->col_idx;
+    g.release = mask_release_counter(mask);
     g.args.list_stride = mask->block_rows;
     g.args.red_blk = mask->m_blk;
     g.args.out_row_blk = mask->k_blk;
@@ -583,20 +681,38 @@ struct sd_layer_plan {
     // runs as one fused launch)
     cudaStream_t aux = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    // launch count right after this plan's last forward and its stream: the
+    // next backward launch may skip the wait for the forward grid if nothing
+    // of ours was launched in between (sd::launch_gemms no_wait)
+    uint64_t fwd_mark = ~0ull;
+    cudaStream_t fwd_stream = nullptr;
 };
 
 namespace {
+// The backward reads X, W, dY and the mask lists and writes dX, dW; the forward
+// reads X, W and the lists and writes Y. So the first backward launch right
+// after the plan's forward (no launch of ours in between, same stream) needs
+// nothing from the forward grid: its CTAs start on the SMs the forward's last
+// wave leaves idle. Any other kernel in between either is one of ours (the
+// count moved: wait) or is an ordinary launch, which the stream already
+// serializes fully. Consumed by the first backward launch.
+bool take_no_wait(sd_layer_plan* plan, cudaStream_t s) {
+    const bool ok = plan->fwd_mark == sd_launch_count() && plan->fwd_stream == s;
+    plan->fwd_mark = ~0ull;
+    return ok;
+}
+
 // The backward's two GEMMs are independent: run them as ONE persistent launch
 // with a shared heaviest-first queue — dX's coarse full-reduction units first,
 // dW's finer units fill the tail.
-void fused_backward(const sd::GemmCall& dx, const sd::GemmCall& dw, cudaStream_t s) {
+void fused_backward(const sd::GemmCall& dx, const sd::GemmCall& dw, cudaStream_t s, bool no_wait) {
     if (sd::tuning() & sd::kTuneNoFusedBackward) {
-        sd::launch_gemm(dw, s);
+        sd::launch_gemm(dw, s, no_wait);
         sd::launch_gemm(dx, s);
         return;
     }
     const sd::GemmCall* calls[2] = {&dx, &dw};
-    sd::launch_gemms(calls, 2, s);
+    sd::launch_gemms(calls, 2, s, no_wait);
 }
 }  // namespace
 
@@ -669,6 +785,11 @@ SD_API int sd_dev_dsd_pairs(const void* a, const void* b, void* c, int32_t c_dty
         launch_gemm2(g.ta, g.tb, g.tout, g.args, pair_cnt, pair_idx, pair_stride, as_stream(stream));
     });
 }
+
+// Development entry (not in the public header): how many mask generations
+// waited on their workspace's reader release counter instead of the whole
+// preceding grid (evidence for the overlap tests).
+SD_API uint64_t sd_dev_mask_counter_waits(void) { return g_counter_waits.load(); }
 
 int sd_linear_forward(const void* x, const sd_block_mask* mask, const void* w, float scale, void* y,
                       int32_t y_dtype, int32_t m, int32_t n, int32_t k, void* stream) {
@@ -755,13 +876,15 @@ int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream) {
         if (!plan) fail(SD_EINVAL, "null plan");
         launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, as_stream(stream));
         launch_gemm(plan_dense(plan) ? plan->dense_fwd : plan->fwd, as_stream(stream));
+        plan->fwd_mark = sd_launch_count();
+        plan->fwd_stream = as_stream(stream);
     });
 }
 
 int sd_layer_plan_backward_dw(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        launch_gemm(plan->dw, as_stream(stream));
+        launch_gemm(plan->dw, as_stream(stream), take_no_wait(plan, as_stream(stream)));
     });
 }
 
@@ -782,22 +905,23 @@ int sd_layer_plan_backward_dw_part(sd_layer_plan* plan, int32_t part, int32_t np
             }
             plan->dw_parts = nparts;
         }
-        launch_gemm(plan->dw_part[part], as_stream(stream));
+        launch_gemm(plan->dw_part[part], as_stream(stream), take_no_wait(plan, as_stream(stream)));
     });
 }
 
 int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        launch_gemm(plan->dx, as_stream(stream));
+        launch_gemm(plan->dx, as_stream(stream), take_no_wait(plan, as_stream(stream)));
     });
 }
 
 int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        if (plan_dense(plan)) fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream));
-        else fused_backward(plan->dx, plan->dw, as_stream(stream));
+        const bool nw = take_no_wait(plan, as_stream(stream));
+        if (plan_dense(plan)) fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), nw);
+        else fused_backward(plan->dx, plan->dw, as_stream(stream), nw);
     });
 }
 
@@ -811,7 +935,7 @@ int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream) {
 int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream));
+        fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), false);
     });
 }
 

@@ -152,6 +152,10 @@ struct LaunchArgs {
     int total_units;
     int trace_id;  // launch sequence number (SD_TRACE timeline)
     unsigned int* sched;  // {next-unit counter, CTAs-done counter}
+    // release counters of the bound mask workspaces this launch reads lists
+    // from (sd_internal.h, reader tracking); null = none
+    unsigned int* release[2];
+    int no_wait;  // skip griddepcontrol.wait (launch_gemms)
 };
 
 struct TensorMaps {
@@ -191,7 +195,7 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         i = head_rows + (u - cu * T);
         half = true;
     }
-    const int rt = a.row_order ? __ldg(a.row_order + i) : i;
+    const int rt = a.row_order ? __ldcg(a.row_order + i) : i;
     t.row0 = rt * kBM;
     t.list_row = t.row0 / a.out_row_blk;
     t.nslots = 0;
@@ -203,7 +207,7 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         t.n0 = cu * width;
         const int rem = a.cols_out - t.n0;
         t.n_eff = rem < width ? (rem > 0 ? rem : 0) : width;
-        const int cnt = a.list_cnt ? __ldg(a.list_cnt + t.list_row) : a.red / a.red_blk;
+        const int cnt = a.list_cnt ? __ldcg(a.list_cnt + t.list_row) : a.red / a.red_blk;
         // this split's contiguous share [lo, hi) of the row's kept blocks
         const int lo = static_cast<int>((static_cast<int64_t>(cnt) * split) / a.splits);
         const int hi = static_cast<int>((static_cast<int64_t>(cnt) * (split + 1)) / a.splits);
@@ -216,14 +220,14 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         // the same unit index also zero-fills the row's DROPPED blocks (kept at
         // the tail of the list by the mask kernel).
         const int per_unit = width / a.out_col_blk;
-        const int cnt = __ldg(a.list_cnt + t.list_row);
+        const int cnt = __ldcg(a.list_cnt + t.list_row);
         const int ndrop = a.mask_cols - cnt;
         const int32_t* row = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride;
         t.n0 = 0;
         for (int j = 0; j < per_unit; ++j) {
             const int li = cu * per_unit + j;
-            if (li < cnt) t.slot_blk[t.nslots++] = __ldg(row + li);
-            if (li < ndrop) t.zero_blk[t.nzero++] = __ldg(row + a.mask_cols - 1 - li);
+            if (li < cnt) t.slot_blk[t.nslots++] = __ldcg(row + li);
+            if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
         }
         t.n_eff = t.nslots * a.out_col_blk;
         t.nstages = a.red / kBK;
@@ -415,8 +419,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // Everything above overlapped the previous kernel's tail (PDL); from here on
-    // we read its outputs (mask lists, operands), so wait for it to complete.
-    ptx::pdl_wait();
+    // we read its outputs (mask lists, operands), so wait for it to complete —
+    // unless the launch is independent of it (no_wait: a plan's backward right
+    // after its forward). Mask lists are read with ld.global.cg (L2), never
+    // through a possibly stale L1 line of an earlier grid.
+    if (!L.no_wait) ptx::pdl_wait();
     ptx::pdl_launch_dependents();
     long long tr[16] = {0};
 #ifdef SD_TRACE
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // kListCap), else read from global one block ahead
                 const int32_t* slist = sched_list + cur_slot * kListCap;
                 const bool staged = cur.nstages / spb <= kListCap;
-                int kb_next = lst ? (staged ? slist[0] : __ldg(lst)) : 0;
+                int kb_next = lst ? (staged ? slist[0] : __ldcg(lst)) : 0;
                 int kb = 0;
                 for (int s = 0, li = 0, sub = 0; s < cur.nstages; ++s) {
                     if (s == claim_at) ptx::mbar_arrive(claim_bar);
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!sdd) {
                         if (sub == 0) {
                             kb = lst ? kb_next : li0 + li;
-                            if (lst && li + 1 < cur.nstages / spb) kb_next = staged ? slist[li + 1] : __ldg(lst + li + 1);
+                            if (lst && li + 1 < cur.nstages / spb) kb_next = staged ? slist[li + 1] : __ldcg(lst + li + 1);
                         }
                         r0 = kb * a.red_blk + sub * kBK;
                         if (++sub == spb) {
@@ -551,6 +558,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::mbar_arrive(sempty_bar + cur_slot);  // done with the slot's staged list
             }
+            // The end marker comes after every unit this CTA decoded (the
+            // scheduler's list/count/order reads) and every list entry this
+            // producer read: the mask workspace may now be regenerated.
+            for (int r = 0; r < 2; ++r) {
+                if (L.release[r]) {
+                    __threadfence();
+                    atomicAdd(L.release[r], 1u);
+                }
+            }
         }
     } else if (warp == 3) {
         // ===================== scheduler =====================
@@ -587,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             nblk = __shfl_sync(0xffffffffu, nblk, 0);
             if (lane == 0) SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
             __syncwarp();
-            for (int i = lane; i < nblk && i < kListCap; i += 32) sched_list[sslot * kListCap + i] = __ldg(src + i);
+            for (int i = lane; i < nblk && i < kListCap; i += 32) sched_list[sslot * kListCap + i] = __ldcg(src + i);
             __syncwarp();
             const int prob = __shfl_sync(0xffffffffu, t.prob, 0);
             if (lane == 0) {
@@ -784,9 +800,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-// Scheduler tuning switches (A/B experiments). Tail halving is off by default:
-// interleaved A/B (tools/ab_tuning.py) showed half-width tail units cost more in
-// operand ingress than they save in idle tail (4096^3: +4% at p=0.5, +11% at p=0.1).
+// Scheduler tuning switches (A/B experiments), all features on by default;
 // SD_TUNING (environment) overrides the default for whole-process A/B runs.
 static int initial_tuning() {
     const char* e = std::getenv("SD_TUNING");
@@ -814,7 +828,7 @@ static bool wide_units(const GemmCall* const* calls, int n) {
     return true;
 }
 
-void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
+void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_wait) {
     if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
     static bool configured = false;
     if (!configured) {
@@ -926,6 +940,13 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     if (grid <= 0) return;
     L.sched = sched_slot();
     L.trace_id = static_cast<int>(sd_launch_count());
+    L.no_wait = no_wait && !(g_tuning & kTuneNoEarlyBackward);
+    // bound mask workspaces read by this launch (lists, counts, row orders)
+    int nrel = 0;
+    for (int i = 0; i < n; ++i) {
+        unsigned int* r = calls[i]->release;
+        if (r && !(nrel > 0 && L.release[0] == r)) L.release[nrel++] = r;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -939,6 +960,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s) {
     if (wide) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<true>, tms, L), "sd_gemm_kernel<wide> launch");
     else check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<false>, tms, L), "sd_gemm_kernel launch");
     note_launch();
+    for (int r = 0; r < nrel; ++r) mask_note_readers(L.release[r], grid, s);
 }
 
 }  // namespace sd

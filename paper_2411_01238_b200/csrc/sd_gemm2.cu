@@ -365,6 +365,12 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel, ta, tb, tout, P), "sd_gemm2_kernel launch");
     note_launch();
+    // this kernel does not release mask workspaces: a following generation
+    // into one it reads waits for the whole grid
+    for (const void* q : {static_cast<const void*>(pair_cnt), static_cast<const void*>(pair_idx),
+                          static_cast<const void*>(g.list_cnt), static_cast<const void*>(g.list_idx),
+                          static_cast<const void*>(g.row_order)})
+        mask_note_untracked(q);
 }
 
 }  // namespace sd

@@ -23,6 +23,23 @@ void check_cuda(cudaError_t e, const char* what);
 int num_sms();
 void note_launch(uint64_t n = 1);
 
+// ---------------------------------------------------------------- mask readers
+// Lets a mask generation overlap the tail of the GEMM that still reads the
+// previous mask of the same workspace (sd_capi.cu, "reader tracking"): every
+// persistent GEMM CTA that reads a bound workspace's lists adds 1 to the
+// workspace's release counter (ticket[1]) once its last list read is done; the
+// next generation into that workspace waits for the count of reader CTAs
+// launched since the previous one instead of for the whole preceding grid.
+void mask_register_workspace(void* ws, size_t bytes, unsigned int* rel);  // sd_mask_bind
+unsigned int* mask_release_counter(const sd_block_mask* m);  // m's counter if m is a live sd_mask_bind binding
+void mask_note_readers(unsigned int* rel, int ctas, cudaStream_t s);  // after a successful launch
+void mask_note_untracked(const void* p);  // a reader that does not release: next generation waits
+// At a generation into the workspace of `rel`: true (and *target) when the
+// generation may wait on the counter instead of griddepcontrol.wait. Resets the
+// workspace's pending count either way (the kernel zeroes the counter).
+bool mask_take_release(unsigned int* rel, cudaStream_t s, uint32_t* target);
+void note_counter_wait();  // a generation launched in counter mode (sd_dev_mask_counter_waits)
+
 // ---------------------------------------------------------------- mask plan
 void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix,
                       uint64_t threshold, cudaStream_t s);
@@ -86,6 +103,7 @@ unsigned int* sched_slot();
 struct GemmCall {
     CUtensorMap ta, tb, tout;
     GemmArgs args;
+    unsigned int* release = nullptr;  // release counter of the mask whose lists args reads (host side)
 };
 
 // Scheduler tuning switches (bitmask; 0 = everything on), for A/B runs.
@@ -97,16 +115,23 @@ enum TuneFlags : int {
     kTuneNoGemm2 = 16,  // dense problems on the 1-CTA kernel instead of the 2-CTA one
     kTuneWide = 32,     // force 128 x 512 units on the 1-CTA kernel
     kTuneNarrow = 64,   // force 128 x 256 units on the 1-CTA kernel
+    kTuneNoEarlyBackward = 128,  // a plan's backward waits for its forward grid (griddepcontrol.wait)
+    kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
 };
 int tuning();
 void set_tuning(int t);
 
 // Launch 1 or 2 independent GEMM problems as ONE persistent kernel sharing a
 // single heaviest-first work queue (problem 0's units are handed out first).
-void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s);
-inline void launch_gemm(const GemmCall& c, cudaStream_t s) {
+// no_wait: the launch reads nothing the immediately preceding grid writes and
+// writes nothing it reads (a plan's backward right after its forward), so its
+// CTAs skip griddepcontrol.wait and start on the SMs the previous grid's tail
+// frees. Every earlier grid is complete by then (the previous grid's CTAs
+// passed their own wait before triggering this launch).
+void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_wait = false);
+inline void launch_gemm(const GemmCall& c, cudaStream_t s, bool no_wait = false) {
     const GemmCall* p = &c;
-    launch_gemms(&p, 1, s);
+    launch_gemms(&p, 1, s, no_wait);
 }
 
 // 2-CTA (cta_group::2) kernel for dense problems (no mask list): 256 x 256

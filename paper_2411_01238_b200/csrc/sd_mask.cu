@@ -13,10 +13,15 @@
 //     popcount of the ballot below the lane, so lists come out strictly
 //     increasing like the reference's.
 // The three parts read nothing but (seed, r, c) — each recomputes the hash — so
-// they run as independent blocks of a single grid; the last block to finish
-// (threadfence + ticket) reduces keep_count and builds the cost-ordered row /
-// column permutations the persistent GEMM scheduler walks (heaviest first).
-// All of this is latency-bound integer work (a 512x64 grid is 4 KB of words).
+// they run as independent blocks of a single grid; keep_count and the
+// cost-ordered row / column permutations the persistent GEMM scheduler walks
+// (heaviest first) come from one extra block that recomputes the counts itself
+// (grids up to 32768 blocks; larger ones: the last block to finish, threadfence
+// + ticket). All of this is latency-bound integer work (a 512x64 grid is 4 KB
+// of words), so it is kept off the layer step's critical path: a generation
+// into a workspace waits only for the reader CTAs of its previous contents to
+// release it (wait_workspace_free), i.e. it runs during the tail of the
+// backward that still finishes on the old mask.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,7 +58,66 @@ struct PlanArgs {
     uint64_t threshold;  // ceil(p * 2^53)
     int nb_words, nb_rows, nb_cols;
     int inline_order;  // one extra block computes counts, keep_count and the orders itself
+    // reader tracking (sd_internal.h): the bound workspace's release counter
+    // (null: not a bound workspace); rel_wait: wait for rel >= rel_target
+    // instead of griddepcontrol.wait
+    unsigned int* rel;
+    uint32_t rel_target;
+    int rel_wait;
 };
+
+__device__ __forceinline__ unsigned long long gclock() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Wait until the previous contents of the workspace are no longer needed.
+// Counter mode: the reader CTAs launched since the last generation have all
+// released (their scheduler/producer list reads are done), so this grid runs
+// during the tail of the GEMM still finishing on the old mask. Bounded: past
+// 20 ms it falls back to griddepcontrol.wait (always sufficient; the bound only
+// matters if the workspace was re-zeroed behind the library's back).
+__device__ __forceinline__ void wait_workspace_free(const PlanArgs& a) {
+    if (!a.rel_wait) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
+    __shared__ int fallback;
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = gclock();
+        int fb = 0;
+        while (true) {
+            unsigned int v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rel) : "memory");
+            if (static_cast<int>(v - a.rel_target) >= 0) break;
+            if (gclock() - t0 > 20000000ull) {
+                fb = 1;
+                break;
+            }
+            __nanosleep(256);
+        }
+        fallback = fb;
+    }
+    __syncthreads();
+    if (fallback) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Exit count for a bound workspace in inline-order mode: the last block out
+// zeroes the release counter for the next round of readers (they can only
+// start releasing after this grid completes).
+__device__ __forceinline__ void finish_block(const PlanArgs& a) {
+    if (!a.rel) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.m.ticket, 1u) == gridDim.x - 1) {
+            *a.rel = 0u;
+            *a.m.ticket = 0u;
+            __threadfence();
+        }
+    }
+}
 
 __device__ __forceinline__ bool keep_bit(const PlanArgs& a, int r, int c) {
     if (a.from_words) {
@@ -135,6 +199,24 @@ __device__ void order_by_count(const int32_t* count, int n, int max_val, int32_t
     __syncthreads();
 }
 
+// Descending order of n <= 64 counts (smem) by one warp: rank = #greater +
+// #equal at a lower index (stable). No block barrier: the row and column
+// orders run in two warps at once (the counting sort above needs ~6 block
+// barriers per order, ~1 us each on the critical path of a layer step).
+__device__ __forceinline__ void warp_rank_order(const int* cnt, int n, int32_t* order) {
+    const int lane = threadIdx.x & 31;
+    const int i0 = lane, i1 = lane + 32;
+    const int v0 = i0 < n ? cnt[i0] : 0, v1 = i1 < n ? cnt[i1] : 0;
+    int r0 = 0, r1 = 0;
+    for (int j = 0; j < n; ++j) {
+        const int w = cnt[j];
+        r0 += (w > v0) | ((w == v0) & (j < i0));
+        r1 += (w > v1) | ((w == v1) & (j < i1));
+    }
+    if (i0 < n) order[r0] = i0;
+    if (i1 < n) order[r1] = i1;
+}
+
 __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     extern __shared__ int dyn_smem[];
     __shared__ int warp_tot[kThreads / 32];
@@ -147,8 +229,9 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(a.trace_id & 255) * 4 + 0], gtimer_m());
 #endif
-    // our own inputs (mask words in compact mode) come from earlier work
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // our own inputs (mask words in compact mode) come from earlier work; in
+    // seed mode only the workspace's previous readers matter
+    wait_workspace_free(a);
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 1], gtimer_m());  // last block past wait
 #endif
@@ -163,42 +246,60 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         int* bins = cc + C;
         for (int i = threadIdx.x; i < R + C; i += kThreads) rc[i] = 0;
         __syncthreads();
-        for (int r = wid; r < R; r += kThreads / 32) {
-            const uint64_t hr = mix64(a.seed_mix ^ static_cast<uint64_t>(r + a.m.row_block_offset));
-            int cnt = 0;
-            for (int c0 = 0; c0 < C; c0 += 32) {
-                const int c = c0 + lane;
-                bool k = false;
-                if (c < C) {
-                    if (a.from_words) {
-                        const int64_t b = static_cast<int64_t>(r) * C + c;
-                        k = (a.m.words[b >> 6] >> (b & 63)) & 1ull;
-                    } else {
-                        k = (mix64(hr ^ static_cast<uint64_t>(c)) >> 11) >= a.threshold;
-                    }
+        // warp w owns rows w, w + 8, ...: row counts accumulate in smem without
+        // atomics, column counts in a register per lane (one smem atomic per
+        // lane and chunk); four rows per pass keep four hash chains in flight
+        constexpr int kW = kThreads / 32;
+        for (int c0 = 0; c0 < C; c0 += 32) {
+            const int c = c0 + lane;
+            int colacc = 0;
+            for (int r = wid; r < R; r += 4 * kW) {
+                bool k[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rr = r + u * kW;
+                    k[u] = c < C && rr < R && keep_bit(a, rr, c);
                 }
-                cnt += __popc(__ballot_sync(0xffffffffu, k));
-                if (k) atomicAdd(&cc[c], 1);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rr = r + u * kW;
+                    const int n = __popc(__ballot_sync(0xffffffffu, k[u]));
+                    if (lane == 0 && rr < R) rc[rr] += n;
+                    colacc += k[u];
+                }
             }
-            if (lane == 0) rc[r] = cnt;
+            if (c < C && colacc) atomicAdd(&cc[c], colacc);
         }
         __syncthreads();
-        unsigned long long kc = 0;
-        for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(rc[r]);
-        for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
-        if (lane == 0) keep_part[wid] = kc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long sum = 0;
-            for (int i = 0; i < kThreads / 32; ++i) sum += keep_part[i];
-            *a.m.keep_count = static_cast<int64_t>(sum);
+        if (R <= 64 && C <= 64) {
+            if (wid == 0) warp_rank_order(rc, R, a.m.row_order);
+            else if (wid == 1) warp_rank_order(cc, C, a.m.col_order);
+            else if (wid == 2) {
+                int kc = 0;
+                for (int r = lane; r < R; r += 32) kc += rc[r];
+                for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+                if (lane == 0) *a.m.keep_count = static_cast<int64_t>(kc);
+            }
+        } else {
+            unsigned long long kc = 0;
+            for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(rc[r]);
+            for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+            if (lane == 0) keep_part[wid] = kc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long sum = 0;
+                for (int i = 0; i < kThreads / 32; ++i) sum += keep_part[i];
+                *a.m.keep_count = static_cast<int64_t>(sum);
+            }
+            order_by_count<true>(rc, R, C, a.m.row_order, bins, warp_tot);
+            order_by_count<true>(cc, C, R, a.m.col_order, bins, warp_tot);
         }
-        order_by_count<true>(rc, R, C, a.m.row_order, bins, warp_tot);
-        order_by_count<true>(cc, C, R, a.m.col_order, bins, warp_tot);
+        __syncthreads();
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef SD_TRACE
-        if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
+        if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 3], gtimer_m());  // order block end
 #endif
+        finish_block(a);
         return;
     }
     if (blk < a.nb_words) {
@@ -280,6 +381,7 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
 #ifdef SD_TRACE
         if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
 #endif
+        finish_block(a);
         return;
     }
 
@@ -309,7 +411,10 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     }
     order_by_count(a.m.row_cnt, R, C, a.m.row_order, dyn_smem, warp_tot);
     order_by_count(a.m.col_cnt, C, R, a.m.col_order, dyn_smem, warp_tot);
-    if (threadIdx.x == 0) *a.m.ticket = 0u;  // re-arm for the next launch on this workspace
+    if (threadIdx.x == 0) {
+        if (a.rel) *a.rel = 0u;  // every block has passed its wait: next round of readers
+        *a.m.ticket = 0u;        // re-arm for the next launch on this workspace
+    }
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
 #endif
@@ -358,6 +463,18 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     a.from_words = from_words ? 1 : 0;
     a.seed_mix = seed_mix;
     a.threshold = threshold;
+    a.rel = mask_release_counter(&m);
+    a.rel_target = 0;
+    a.rel_wait = 0;
+    if (a.rel) {
+        uint32_t target = 0;
+        const bool ok = mask_take_release(a.rel, s, &target);
+        if (ok && !from_words && !(tuning() & kTuneNoMaskOverlap)) {
+            a.rel_wait = 1;
+            a.rel_target = target;
+            note_counter_wait();
+        }
+    }
     const int64_t nwords = (static_cast<int64_t>(m.block_rows) * m.block_cols + 63) / 64;
     a.nb_words = from_words ? 0 : static_cast<int>((nwords + kThreads / 32 - 1) / (kThreads / 32));
     a.nb_rows = (m.block_rows + kThreads / 32 - 1) / (kThreads / 32);

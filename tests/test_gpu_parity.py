@@ -93,6 +93,9 @@ def test_mask_bit_exact(sd, oracle, rows, cols, seed, p):
     ro = m.row_order_device().cpu().numpy()
     assert sorted(ro.tolist()) == list(range(R))
     assert all(rc[ro[i]] >= rc[ro[i + 1]] for i in range(R - 1))  # heaviest first
+    co = m.col_order_device().cpu().numpy()
+    assert sorted(co.tolist()) == list(range(C))
+    assert all(cc[co[i]] >= cc[co[i + 1]] for i in range(C - 1))
 
 
 def test_mask_golden(sd, golden):
