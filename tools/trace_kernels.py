@@ -1,7 +1,7 @@
 """Wait-cycle attribution for the GEMM kernel (dev tool; needs `make trace`).
 
   SPARSEDROP_B200_LIB=paper_2411_01238_b200/lib/libsparsedrop_b200_trace.so \
-      python tools/trace_kernels.py SIZE P
+      python tools/trace_kernels.py SIZE|M,N,K P
 For each kernel: mean per-CTA cycles of the MMA thread's run, of its waits for
 data (full), for TMEM (epilogue) and for the scheduler, the producer's waits for
 free stages, and the epilogue's waits — as fractions of the MMA thread's run."""
@@ -19,9 +19,9 @@ import paper_2411_01238_b200 as sd  # noqa: E402
 
 lib = sd.load_library()
 lib.sd_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
-S = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+S = sys.argv[1] if len(sys.argv) > 1 else "4096"
 P = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
-M = N = K = S
+M, N, K = (int(v) for v in S.split(",")) if "," in S else (int(S),) * 3
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 w = torch.randn(K, N, device="cuda").to(torch.bfloat16)
 dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
