@@ -189,13 +189,13 @@ unsigned int* sched_slot() {
         std::lock_guard<std::mutex> lock(mu);
         if (!slots[dev]) {
             unsigned int* p = nullptr;
-            check_cuda(cudaMalloc(&p, kSlots * 2 * sizeof(unsigned int)), "cudaMalloc(scheduler slots)");
-            check_cuda(cudaMemset(p, 0, kSlots * 2 * sizeof(unsigned int)), "cudaMemset(scheduler slots)");
+            check_cuda(cudaMalloc(&p, kSlots * 4 * sizeof(unsigned int)), "cudaMalloc(scheduler slots)");
+            check_cuda(cudaMemset(p, 0, kSlots * 4 * sizeof(unsigned int)), "cudaMemset(scheduler slots)");
             check_cuda(cudaDeviceSynchronize(), "scheduler slots init");
             slots[dev] = p;
         }
     }
-    return slots[dev] + 2 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
+    return slots[dev] + 4 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
 }
 
 // ---------------------------------------------------------------- reader tracking

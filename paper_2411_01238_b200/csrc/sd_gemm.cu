@@ -151,11 +151,15 @@ struct LaunchArgs {
     int nprob;
     int total_units;
     int trace_id;  // launch sequence number (SD_TRACE timeline)
-    unsigned int* sched;  // {next-unit counter, CTAs-done counter}
+    unsigned int* sched;  // {next-unit counter, CTAs-done counter, units-decoded counter, -}
     // release counters of the bound mask workspaces this launch reads lists
     // from (sd_internal.h, reader tracking); null = none
     unsigned int* release[2];
     int no_wait;  // skip griddepcontrol.wait (launch_gemms)
+    // 1: no unit's list can exceed the smem staging, so the mask workspaces are
+    // free once every unit is decoded: the CTA that decodes the last unit
+    // releases for the whole grid. 0: each CTA releases when it stops reading.
+    int release_all;
 };
 
 struct TensorMaps {
@@ -233,6 +237,16 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         t.nstages = a.red / kBK;
     }
     return t;
+}
+
+// This CTA is done reading the mask workspaces of the launch (release counters).
+__device__ __forceinline__ void release_workspaces(const LaunchArgs& L) {
+    for (int r = 0; r < 2; ++r) {
+        if (L.release[r]) {
+            __threadfence();
+            atomicAdd(L.release[r], 1u);
+        }
+    }
 }
 
 template <bool WIDE>
@@ -456,6 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (cur.prob < 0) {
                     ptx::mbar_arrive(sempty_bar + cur_slot);
+                    // lists were read here (units too long to stage): the mask
+                    // workspace is released now that every load is issued
+                    if (cur.nslots) release_workspaces(L);
                     break;
                 }
                 const int nst = cur.n_eff == 0 ? 0 : cur.nstages;
@@ -558,15 +575,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::mbar_arrive(sempty_bar + cur_slot);  // done with the slot's staged list
             }
-            // The end marker comes after every unit this CTA decoded (the
-            // scheduler's list/count/order reads) and every list entry this
-            // producer read: the mask workspace may now be regenerated.
-            for (int r = 0; r < 2; ++r) {
-                if (L.release[r]) {
-                    __threadfence();
-                    atomicAdd(L.release[r], 1u);
-                }
-            }
         }
     } else if (warp == 3) {
         // ===================== scheduler =====================
@@ -584,10 +592,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sphase = 0;
         uint32_t cphase = 0;
         int u = blockIdx.x;
+        bool unstaged = false;  // a unit's list was too long to stage: the producer reads it
         while (true) {
             Unit t;
             if (lane == 0) {
-                if (u < num_units) t = decode_global<WIDE>(L, u); else t.prob = -1;
+                if (u < num_units) {
+                    t = decode_global<WIDE>(L, u);
+                } else {
+                    t.prob = -1;
+                    t.nslots = unstaged ? 1 : 0;  // end marker: who releases the mask workspace
+                }
             }
             // list source of this unit (dsd with a list): entries [li0, li0 + nblk)
             const int32_t* src = nullptr;
@@ -601,11 +615,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), 0));
             nblk = __shfl_sync(0xffffffffu, nblk, 0);
+            unstaged = unstaged || nblk > kListCap;
             if (lane == 0) SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
             __syncwarp();
             for (int i = lane; i < nblk && i < kListCap; i += 32) sched_list[sslot * kListCap + i] = __ldcg(src + i);
             __syncwarp();
             const int prob = __shfl_sync(0xffffffffu, t.prob, 0);
+            // the last unit of the launch decoded: nothing reads the mask
+            // workspaces any more (every other unit was decoded before its
+            // counter increment), whatever the CTAs still have to compute
+            if (L.release_all && prob >= 0 && lane == 0 &&
+                atomicAdd(L.sched + 2, 1u) == static_cast<unsigned int>(num_units) - 1u) {
+                for (int r = 0; r < 2; ++r) {
+                    if (L.release[r]) {
+                        __threadfence();
+                        atomicAdd(L.release[r], gridDim.x);
+                    }
+                }
+            }
             if (lane == 0) {
                 sched_unit[sslot] = t;
                 ptx::mbar_arrive(sfull_bar + sslot);  // release: the list stores above are visible
@@ -614,7 +641,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sslot = 0;
                 sphase ^= 1;
             }
-            if (prob < 0) break;
+            if (prob < 0) {
+                // Every unit this CTA will run is decoded and its list staged in
+                // smem: the mask workspace (lists, counts, row order) is no longer
+                // read, so the next generation into it may start (reader
+                // tracking, sd_internal.h) while this CTA's last units still run.
+                if (lane == 0 && !unstaged && !L.release_all) release_workspaces(L);
+                break;
+            }
             if (lane == 0) {
                 ptx::mbar_wait(claim_bar, cphase);
                 u = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
@@ -793,6 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (atomicAdd(L.sched + 1, 1u) == gridDim.x - 1) {
             L.sched[0] = 0u;
             L.sched[1] = 0u;
+            L.sched[2] = 0u;
             __threadfence();
         }
     }
@@ -943,10 +978,14 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     L.no_wait = no_wait && !(g_tuning & kTuneNoEarlyBackward);
     // bound mask workspaces read by this launch (lists, counts, row orders)
     int nrel = 0;
+    bool may_unstage = false;  // a dsd list longer than the scheduler's smem staging
     for (int i = 0; i < n; ++i) {
         unsigned int* r = calls[i]->release;
         if (r && !(nrel > 0 && L.release[0] == r)) L.release[nrel++] = r;
+        const GemmArgs& a = L.p[i];
+        if (!(a.flags & kFlagSDD) && a.list_idx && a.red / a.red_blk > kListCap) may_unstage = true;
     }
+    L.release_all = may_unstage ? 0 : 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);

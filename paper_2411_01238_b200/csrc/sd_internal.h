@@ -95,8 +95,9 @@ inline int gemm_units(const GemmArgs& a) {
     return ((a.n_row_tiles - T) * a.n_col_units + T * 2 * a.n_col_units) * (a.splits > 0 ? a.splits : 1);
 }
 
-// A zeroed {counter, done} pair for one persistent-kernel launch (ring of
-// slots per device, re-armed by the last CTA of the launch that used it).
+// Zeroed {next unit, CTAs done, units decoded, spare} counters for one
+// persistent-kernel launch (ring of slots per device, re-armed by the last CTA
+// of the launch that used it).
 unsigned int* sched_slot();
 
 // A fully validated, ready-to-launch GEMM problem (tensor maps encoded).

@@ -225,16 +225,25 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     const int R = a.m.block_rows, C = a.m.block_cols;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    int blk = blockIdx.x;
+    // the order block (the longest) is block 0 so it is dispatched first when
+    // SMs free up at the end of the previous GEMM
+    int blk = a.inline_order ? (blockIdx.x == 0 ? a.nb_words + a.nb_rows + a.nb_cols : blockIdx.x - 1)
+                             : static_cast<int>(blockIdx.x);
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMin(&g_sd_timeline[(a.trace_id & 255) * 4 + 0], gtimer_m());
-#endif
-    // our own inputs (mask words in compact mode) come from earlier work; in
-    // seed mode only the workspace's previous readers matter
-    wait_workspace_free(a);
-#ifdef SD_TRACE
+#define SD_PAST_WAIT() \
     if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 1], gtimer_m());  // last block past wait
+#else
+#define SD_PAST_WAIT()
 #endif
+    // Compact mode reads the given words, written by earlier work: wait first.
+    // Seed mode reads nothing, so every block computes its part first and waits
+    // (for the workspace's previous readers) only before its first global write.
+    const bool early = !a.from_words;
+    if (!early) {
+        wait_workspace_free(a);
+        SD_PAST_WAIT()
+    }
 
     if (a.inline_order && blk == a.nb_words + a.nb_rows + a.nb_cols) {
         // ---- counts, keep_count and cost orders, recomputed by this block alone
@@ -243,7 +252,9 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         // critical path (that phase cost 4-8 us per mask, ~3% of a 4096^3 step).
         int* rc = dyn_smem;
         int* cc = rc + R;
-        int* bins = cc + C;
+        int* ro = cc + C;   // fast path: orders staged here until the wait
+        int* co = ro + R;
+        int* bins = co + C;
         for (int i = threadIdx.x; i < R + C; i += kThreads) rc[i] = 0;
         __syncthreads();
         // warp w owns rows w, w + 8, ...: row counts accumulate in smem without
@@ -272,15 +283,26 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         }
         __syncthreads();
         if (R <= 64 && C <= 64) {
-            if (wid == 0) warp_rank_order(rc, R, a.m.row_order);
-            else if (wid == 1) warp_rank_order(cc, C, a.m.col_order);
-            else if (wid == 2) {
+            if (wid == 0) warp_rank_order(rc, R, ro);
+            else if (wid == 1) warp_rank_order(cc, C, co);
+            __syncthreads();
+            if (early) {
+                wait_workspace_free(a);
+                SD_PAST_WAIT()
+            }
+            for (int i = threadIdx.x; i < R; i += kThreads) a.m.row_order[i] = ro[i];
+            for (int i = threadIdx.x; i < C; i += kThreads) a.m.col_order[i] = co[i];
+            if (wid == 2) {
                 int kc = 0;
                 for (int r = lane; r < R; r += 32) kc += rc[r];
                 for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
                 if (lane == 0) *a.m.keep_count = static_cast<int64_t>(kc);
             }
         } else {
+            if (early) {
+                wait_workspace_free(a);
+                SD_PAST_WAIT()
+            }
             unsigned long long kc = 0;
             for (int r = threadIdx.x; r < R; r += kThreads) kc += static_cast<unsigned long long>(rc[r]);
             for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
@@ -307,26 +329,46 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         const int64_t total = static_cast<int64_t>(R) * C;
         const int64_t nwords = (total + 63) / 64;
         const int64_t w = static_cast<int64_t>(blk) * (kThreads / 32) + wid;
+        uint64_t word = 0;
         if (w < nwords) {
             const int64_t b0 = w * 64 + lane, b1 = b0 + 32;
             const bool k0 = b0 < total && keep_bit(a, static_cast<int>(b0 / C), static_cast<int>(b0 % C));
             const bool k1 = b1 < total && keep_bit(a, static_cast<int>(b1 / C), static_cast<int>(b1 % C));
             const uint32_t lo = __ballot_sync(0xffffffffu, k0);
             const uint32_t hi = __ballot_sync(0xffffffffu, k1);
-            if (lane == 0) a.m.words[w] = (static_cast<uint64_t>(hi) << 32) | lo;
+            word = (static_cast<uint64_t>(hi) << 32) | lo;
         }
+        if (early) {
+            wait_workspace_free(a);
+            SD_PAST_WAIT()
+        }
+        if (w < nwords && lane == 0) a.m.words[w] = word;
     } else if ((blk -= a.nb_words) < a.nb_rows) {
         // ---- row lists: one warp per block row. Kept columns ascending from the
         // front (kept_blocks_in_row), dropped columns from the back (the sdd
-        // kernel's zero-fill list).
+        // kernel's zero-fill list). Keep bits of up to 32 column chunks are held
+        // in a register across the wait.
         const int r = blk * (kThreads / 32) + wid;
+        const int nch = (C + 31) / 32;
+        const bool held = early && nch <= 32;
+        uint32_t kbits = 0;
+        if (held && r < R) {
+            for (int j = 0; j < nch; ++j) {
+                const int c = j * 32 + lane;
+                kbits |= static_cast<uint32_t>(c < C && keep_bit(a, r, c)) << j;
+            }
+        }
+        if (early) {
+            wait_workspace_free(a);
+            SD_PAST_WAIT()
+        }
         if (r < R) {
             int base = 0, dbase = 0;
             int32_t* dst = a.m.row_idx + static_cast<int64_t>(r) * C;
-            for (int c0 = 0; c0 < C; c0 += 32) {
+            for (int j = 0, c0 = 0; c0 < C; ++j, c0 += 32) {
                 const int c = c0 + lane;
                 const bool valid = c < C;
-                const bool k = valid && keep_bit(a, r, c);
+                const bool k = valid && (held ? ((kbits >> j) & 1u) : keep_bit(a, r, c));
                 const uint32_t bal = __ballot_sync(0xffffffffu, k);
                 const uint32_t dbal = __ballot_sync(0xffffffffu, valid && !k);
                 if (k) dst[base + __popc(bal & lt)] = c;
@@ -355,6 +397,10 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
         }
         if (lane == 0) warp_tot[wid] = cnt;
         __syncthreads();
+        if (early) {
+            wait_workspace_free(a);
+            SD_PAST_WAIT()
+        }
         int base = 0;
         for (int i = 0; i < wid; ++i) base += warp_tot[i];
         int32_t* dst = a.m.col_idx + static_cast<int64_t>(c) * R;
@@ -487,7 +533,7 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     const int grid = a.nb_words + a.nb_rows + a.nb_cols + a.inline_order;
     const int bins = std::min(std::max(m.block_rows, m.block_cols) + 1, kMaxOrderBins);
     const int chunks = (m.block_rows + 31) / 32;
-    const int inline_ints = a.inline_order ? m.block_rows + m.block_cols + bins : 0;
+    const int inline_ints = a.inline_order ? 2 * (m.block_rows + m.block_cols) + bins : 0;
     const size_t smem = static_cast<size_t>(std::max({bins, chunks, inline_ints})) * sizeof(int);
     if (smem > 48 * 1024) {
         static bool raised = false;
