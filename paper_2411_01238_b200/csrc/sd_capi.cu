@@ -686,6 +686,7 @@ struct sd_layer_plan {
     // of ours was launched in between (sd::launch_gemms no_wait)
     uint64_t fwd_mark = ~0ull;
     cudaStream_t fwd_stream = nullptr;
+    bool early_backward = true;  // false when buffers alias (sd_layer_plan_create)
 };
 
 namespace {
@@ -697,7 +698,7 @@ namespace {
 // count moved: wait) or is an ordinary launch, which the stream already
 // serializes fully. Consumed by the first backward launch.
 bool take_no_wait(sd_layer_plan* plan, cudaStream_t s) {
-    const bool ok = plan->fwd_mark == sd_launch_count() && plan->fwd_stream == s;
+    const bool ok = plan->early_backward && plan->fwd_mark == sd_launch_count() && plan->fwd_stream == s;
     plan->fwd_mark = ~0ull;
     return ok;
 }
@@ -860,6 +861,30 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
         tmp.x = x;
         tmp.m = m, tmp.n = n, tmp.k = k;
+        // the early backward relies on the forward writing nothing the backward
+        // touches: with Y overlapping X, W, dY, dX or dW, or the mask workspace
+        // overlapping any buffer, every backward waits for the forward grid
+        {
+            const auto el = [](int dt) -> size_t { return dt == SD_DTYPE_F32 ? 4 : 2; };
+            struct Range {
+                uintptr_t b, e;
+            };
+            const auto rg = [](const void* p, size_t bytes) {
+                return Range{reinterpret_cast<uintptr_t>(p), reinterpret_cast<uintptr_t>(p) + bytes};
+            };
+            const Range ry = rg(y, static_cast<size_t>(m) * n * el(y_dtype));
+            const Range others[5] = {rg(x, static_cast<size_t>(m) * k * 2), rg(w, static_cast<size_t>(k) * n * 2),
+                                     rg(dy, static_cast<size_t>(m) * n * 2),
+                                     rg(dx, static_cast<size_t>(m) * k * el(dx_dtype)),
+                                     rg(dw, static_cast<size_t>(k) * n * el(dw_dtype))};
+            const size_t mws = sd_mask_workspace_bytes(mask->block_rows, mask->block_cols);
+            const Range rm = rg(mask->words, mws);
+            const auto overlap = [](Range a, Range b) { return a.b < b.e && b.b < a.e; };
+            bool alias = false;
+            for (const Range& o : others) alias = alias || overlap(ry, o) || overlap(rm, o);
+            alias = alias || overlap(rm, ry);
+            tmp.early_backward = !alias;
+        }
         *out = new sd_layer_plan(tmp);
     });
 }

@@ -858,6 +858,10 @@ static bool wide_units(const GemmCall* const* calls, int n) {
     for (int i = 0; i < n; ++i) {
         const GemmArgs& a = calls[i]->args;
         if ((a.flags & kFlagSDD) || a.cols_out <= kBN) return false;
+        // a ragged 256-column unit per row costs a whole single-buffered wide
+        // accumulator: the ViT fc2 forward (N = 768) is 3-5% faster narrow
+        // (profiles/r01_cfg3_width_ab.txt)
+        if (a.cols_out % (2 * kBN) != 0 && a.cols_out < 8 * kBN) return false;
         if (a.keep_hint >= 0.f && a.keep_hint < 0.2f) return false;
     }
     return true;

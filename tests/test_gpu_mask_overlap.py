@@ -199,3 +199,41 @@ def test_overlap_switches_do_not_change_results(sd):
     finally:
         P.lib.sd_set_tuning(0)
         P.close()
+
+
+def test_aliased_buffers_keep_the_backward_waiting(sd):
+    """dY aliasing Y (the forward's output is the backward's input): the plan
+    must not start its backward before the forward grid completes."""
+    from paper_2411_01238_b200._capi import SdBlockMask
+
+    lib = sd.load_library()
+    M = N = K = 2048
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(K, N, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    ydy = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    dx = torch.empty(M, K, dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty(K, N, dtype=torch.float32, device="cuda")
+    ws, mask = _bound_mask(lib, SdBlockMask, M // 128, K // 128)
+    plan = ctypes.c_void_p()
+    assert lib.sd_layer_plan_create(ctypes.byref(plan), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                    ctypes.c_void_p(ydy.data_ptr()), ctypes.c_void_p(ydy.data_ptr()), 1,
+                                    ctypes.c_void_p(dx.data_ptr()), 1, ctypes.c_void_p(dw.data_ptr()), 0, M, N, K,
+                                    ctypes.c_double(0.5), ctypes.byref(mask)) == 0
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    try:
+        res = []
+        for sync in (False, True):
+            for rep in range(3):
+                ydy.zero_()
+                assert lib.sd_layer_plan_forward(plan, ctypes.c_uint64(77), st) == 0
+                if sync:
+                    torch.cuda.synchronize()
+                assert lib.sd_layer_plan_backward(plan, st) == 0
+                torch.cuda.synchronize()
+                res.append((dx.clone(), dw.clone()))
+        for a, b in res[1:]:
+            assert torch.equal(a, res[0][0]) and torch.equal(b, res[0][1])
+        assert res[0][1].abs().sum() > 0
+    finally:
+        lib.sd_layer_plan_destroy(plan)
