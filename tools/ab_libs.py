@@ -1,6 +1,6 @@
 """Interleaved A/B of two builds of libsparsedrop_b200.so in ONE process (dev tool).
 
-    python tools/ab_libs.py LIB_A[:tuning] LIB_B[:tuning] [SIZE] [P] [rounds]
+    python tools/ab_libs.py LIB_A[:tuning] LIB_B[:tuning] [SIZE|M,N,K] [P] [rounds]
 
 Both libraries are loaded side by side (RTLD_LOCAL) and bound to the same
 operand buffers through their own layer plans; each round times forward,
@@ -39,11 +39,11 @@ def load(spec):
     return lib
 
 
-S = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
+S = sys.argv[3] if len(sys.argv) > 3 else "4096"  # SIZE or M,N,K
 P = float(sys.argv[4]) if len(sys.argv) > 4 else 0.5
 rounds = int(sys.argv[5]) if len(sys.argv) > 5 else 8
 libs = [load(sys.argv[1]), load(sys.argv[2])]
-M = N = K = S
+M, N, K = (int(v) for v in S.split(",")) if "," in S else (int(S),) * 3
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 w = torch.randn(K, N, device="cuda").to(torch.bfloat16)
 dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
