@@ -677,10 +677,6 @@ struct sd_layer_plan {
     int dw_parts = 0;
     const void* x = nullptr;
     int m = 0, n = 0, k = 0;
-    // (kept for ABI compatibility of the plan object; unused since the backward
-    // runs as one fused launch)
-    cudaStream_t aux = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
     // launch count right after this plan's last forward and its stream: the
     // next backward launch may skip the wait for the forward grid if nothing
     // of ours was launched in between (sd::launch_gemms no_wait)
@@ -965,11 +961,6 @@ int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
 }
 
 int sd_layer_plan_destroy(sd_layer_plan* plan) {
-    if (plan) {
-        if (plan->aux) cudaStreamDestroy(plan->aux);
-        if (plan->fork) cudaEventDestroy(plan->fork);
-        if (plan->join) cudaEventDestroy(plan->join);
-    }
     delete plan;
     return SD_OK;
 }
