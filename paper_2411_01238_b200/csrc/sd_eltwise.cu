@@ -81,15 +81,19 @@ __global__ void __launch_bounds__(kThreads) gelu_fwd_kernel(const uint4* __restr
     }
 }
 
+// d GELU / dh = Phi(h) + h phi(h), one explicit FMA so the direct kernel and
+// the table builder below round identically
+__device__ __forceinline__ float gelu_dgrad(float x) {
+    const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
+    return __fmaf_rn(x, pdf, phi_cdf(x));
+}
+
 __device__ __forceinline__ uint4 gelu_bwd8(const uint4& hv, const uint4& gv) {
     float x[8], gr[8];
     unpack8(hv, x);
     unpack8(gv, gr);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const float pdf = 0.3989422804014327f * __expf(-0.5f * x[j] * x[j]);
-        gr[j] = gr[j] * (phi_cdf(x[j]) + x[j] * pdf);
-    }
+    for (int j = 0; j < 8; ++j) gr[j] = gr[j] * gelu_dgrad(x[j]);
     return pack8(gr);
 }
 
@@ -110,34 +114,47 @@ __global__ void __launch_bounds__(kThreads) gelu_bwd_kernel(const uint4* __restr
     for (; i < n8; i += stride) dh[i] = gelu_bwd8(ld_nc(h + i), ld_nc(g + i));
 }
 
-// GELU of every bf16 bit pattern, with exactly gelu_fwd_kernel's math: the
-// activation of a bf16 input is a 64 K-entry table. The forward then reads a
-// 128 KB shared-memory copy instead of evaluating erff per element (the
-// evaluating kernel is ALU-bound at ~3.6 TB/s effective); outputs are identical.
-__global__ void __launch_bounds__(kThreads) gelu_lut_build_kernel(uint16_t* lut) {
-    const int v = blockIdx.x * kThreads + threadIdx.x;
-    if (v >= 65536) return;
-    const float x = __uint_as_float(static_cast<uint32_t>(v) << 16);
+// Forward table: GELU of the bf16 inputs with exponent field in
+// [kDE0, kDE0 + kDNE) (2^-31 <= |h| < 2^33), with exactly gelu_fwd_kernel's
+// math, as bf16: 16 K entries, 32 KB of shared memory, so three 512-thread
+// CTAs fit per SM (the 64 K-entry, 128 KB table held one, 4.9 TB/s). Inputs
+// outside the range are evaluated directly: outputs are identical either way.
+constexpr int kDE0 = 96, kDNE = 64;
+constexpr int kDPerSign = kDNE * 128;
+constexpr int kLutThreads = 512;
+constexpr int kLutBytes = 2 * kDPerSign * 2;
+
+__device__ __forceinline__ uint32_t gelu_bf16_bits(float x) {
     const __nv_bfloat162 r = __floats2bfloat162_rn(x * phi_cdf(x), 0.0f);
-    lut[v] = *reinterpret_cast<const uint16_t*>(&r);
+    return *reinterpret_cast<const uint16_t*>(&r);
 }
 
-constexpr int kLutThreads = 512;
-constexpr int kLutBytes = 65536 * 2;
+__global__ void __launch_bounds__(kThreads) gelu_lut_build_kernel(uint16_t* lut) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= 2 * kDPerSign) return;
+    const uint32_t sign = static_cast<uint32_t>(i / kDPerSign);
+    const uint32_t a = static_cast<uint32_t>(i % kDPerSign) + (kDE0 << 7);
+    lut[i] = static_cast<uint16_t>(gelu_bf16_bits(__uint_as_float(((sign << 15) | a) << 16)));
+}
 
-__global__ void __launch_bounds__(kLutThreads, 1) gelu_fwd_lut_kernel(const uint4* __restrict__ h,
+__global__ void __launch_bounds__(kLutThreads, 3) gelu_fwd_lut_kernel(const uint4* __restrict__ h,
                                                                      uint4* __restrict__ act, int64_t n8,
                                                                      const uint4* __restrict__ lut) {
     extern __shared__ uint4 lut_s4[];
     for (int i = threadIdx.x; i < kLutBytes / 16; i += kLutThreads) lut_s4[i] = __ldg(lut + i);
     __syncthreads();
     const uint16_t* t = reinterpret_cast<const uint16_t*>(lut_s4);
+    const auto one = [&](uint32_t v) -> uint32_t {
+        const uint32_t off = (v & 0x7FFFu) - (kDE0 << 7);
+        return off < static_cast<uint32_t>(kDPerSign) ? t[(v >> 15) * kDPerSign + off]
+                                                      : gelu_bf16_bits(__uint_as_float(v << 16));
+    };
     auto apply = [&](const uint4& v) {
         uint4 o;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
         uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ow[j] = static_cast<uint32_t>(t[w[j] & 0xFFFFu]) | (static_cast<uint32_t>(t[w[j] >> 16]) << 16);
+        for (int j = 0; j < 4; ++j) ow[j] = one(w[j] & 0xFFFFu) | (one(w[j] >> 16) << 16);
         return o;
     };
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kLutThreads;
@@ -150,6 +167,82 @@ __global__ void __launch_bounds__(kLutThreads, 1) gelu_fwd_lut_kernel(const uint
         for (int u = 0; u < kUnroll; ++u) act[i + u * stride] = apply(v[u]);
     }
     for (; i < n8; i += stride) act[i] = apply(ld_nc(h + i));
+}
+
+// Backward table: d GELU / dh (fp32, exactly gelu_dgrad) of the bf16 inputs
+// with exponent field in [kDE0, kDE0 + kDNE), i.e. 2^-31 <= |h| < 2^33 —
+// 16 K entries, 64 KB of shared memory, two CTAs per SM. Inputs outside the
+// range (tiny, huge, NaN/Inf) are evaluated directly: same bits either way.
+constexpr int kDLutBytes = 2 * kDPerSign * 4;
+constexpr int kDThreads = 512;
+
+__global__ void __launch_bounds__(kThreads) gelu_dlut_build_kernel(float* lut) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= 2 * kDPerSign) return;
+    const uint32_t sign = static_cast<uint32_t>(i / kDPerSign);
+    const uint32_t a = static_cast<uint32_t>(i % kDPerSign) + (kDE0 << 7);
+    const float x = __uint_as_float(((sign << 15) | a) << 16);
+    lut[i] = gelu_dgrad(x);
+}
+
+__global__ void __launch_bounds__(kDThreads, 2) gelu_bwd_lut_kernel(const uint4* __restrict__ h,
+                                                                    const uint4* __restrict__ g,
+                                                                    uint4* __restrict__ dh, int64_t n8,
+                                                                    const float4* __restrict__ lut) {
+    extern __shared__ float4 dlut_s4[];
+    for (int i = threadIdx.x; i < kDLutBytes / 16; i += kDThreads) dlut_s4[i] = __ldg(lut + i);
+    __syncthreads();
+    const float* t = reinterpret_cast<const float*>(dlut_s4);
+    auto apply = [&](const uint4& hv, const uint4& gv) {
+        float gr[8];
+        unpack8(gv, gr);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&hv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t v = (w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+            const uint32_t off = (v & 0x7FFFu) - (kDE0 << 7);
+            const float d = off < static_cast<uint32_t>(kDPerSign) ? t[(v >> 15) * kDPerSign + off]
+                                                                    : gelu_dgrad(__uint_as_float(v << 16));
+            gr[j] = gr[j] * d;
+        }
+        return pack8(gr);
+    };
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDThreads;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kDThreads + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n8; i += kUnroll * stride) {
+        uint4 hv[kUnroll], gv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            hv[u] = ld_nc(h + i + u * stride);
+            gv[u] = ld_nc(g + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) dh[i + u * stride] = apply(hv[u], gv[u]);
+    }
+    for (; i < n8; i += stride) dh[i] = apply(ld_nc(h + i), ld_nc(g + i));
+}
+
+const float4* gelu_dlut() {
+    static float* luts[64] = {nullptr};
+    static std::mutex mu;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) fail(SD_ERUNTIME, "device index out of range");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!luts[dev]) {
+        float* p = nullptr;
+        check_cuda(cudaMalloc(&p, kDLutBytes), "cudaMalloc(GELU' table)");
+        cudaStream_t s;
+        check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        gelu_dlut_build_kernel<<<(2 * kDPerSign + kThreads - 1) / kThreads, kThreads, 0, s>>>(p);
+        check_cuda(cudaGetLastError(), "GELU' table build");
+        check_cuda(cudaStreamSynchronize(s), "GELU' table build");
+        cudaStreamDestroy(s);
+        check_cuda(cudaFuncSetAttribute(gelu_bwd_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDLutBytes),
+                   "GELU' kernel smem");
+        luts[dev] = p;
+    }
+    return reinterpret_cast<const float4*>(luts[dev]);
 }
 
 // The table, built once per device (synchronously, before first use).
@@ -165,7 +258,7 @@ const uint4* gelu_lut() {
         check_cuda(cudaMalloc(&p, kLutBytes), "cudaMalloc(GELU table)");
         cudaStream_t s;
         check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-        gelu_lut_build_kernel<<<65536 / kThreads, kThreads, 0, s>>>(p);
+        gelu_lut_build_kernel<<<(2 * kDPerSign + kThreads - 1) / kThreads, kThreads, 0, s>>>(p);
         check_cuda(cudaGetLastError(), "GELU table build");
         check_cuda(cudaStreamSynchronize(s), "GELU table build");
         cudaStreamDestroy(s);
@@ -200,8 +293,8 @@ int sd_gelu_forward(const void* h, void* act, int64_t n, void* stream) {
         const uint4* lut = gelu_lut();
         const int64_t n8 = n / 8;
         if (n8 >= 65536) {
-            // large activations: the table kernel (one 128 KB smem copy per SM)
-            gelu_fwd_lut_kernel<<<num_sms(), kLutThreads, kLutBytes, static_cast<cudaStream_t>(stream)>>>(
+            // large activations: the table kernel (a 32 KB smem copy per CTA)
+            gelu_fwd_lut_kernel<<<3 * num_sms(), kLutThreads, kLutBytes, static_cast<cudaStream_t>(stream)>>>(
                 static_cast<const uint4*>(h), static_cast<uint4*>(act), n8, lut);
         } else {
             gelu_fwd_kernel<<<grid_for(n8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -219,8 +312,21 @@ int sd_gelu_backward(const void* h, const void* grad, void* dh, int64_t n, void*
         reinterpret_cast<uintptr_t>(grad) % 16 || reinterpret_cast<uintptr_t>(dh) % 16)
         return SD_EINVAL;
     if (n == 0) return SD_OK;
-    gelu_bwd_kernel<<<grid_for(n / 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(h), static_cast<const uint4*>(grad), static_cast<uint4*>(dh), n / 8);
+    const int64_t n8 = n / 8;
+    if (n8 >= 65536 && !(tuning() & kTuneNoGeluTable)) {
+        // large activations: d GELU / dh from a 64 KB shared-memory table
+        const float4* lut = nullptr;
+        try {
+            lut = gelu_dlut();
+        } catch (const Error&) {
+            return SD_ERUNTIME;
+        }
+        gelu_bwd_lut_kernel<<<2 * num_sms(), kDThreads, kDLutBytes, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const uint4*>(h), static_cast<const uint4*>(grad), static_cast<uint4*>(dh), n8, lut);
+    } else {
+        gelu_bwd_kernel<<<grid_for(n8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const uint4*>(h), static_cast<const uint4*>(grad), static_cast<uint4*>(dh), n8);
+    }
     note_launch();
     return cudaGetLastError() == cudaSuccess ? SD_OK : SD_ERUNTIME;
 }

@@ -118,6 +118,7 @@ enum TuneFlags : int {
     kTuneNarrow = 64,   // force 128 x 256 units on the 1-CTA kernel
     kTuneNoEarlyBackward = 128,  // a plan's backward waits for its forward grid (griddepcontrol.wait)
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
+    kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
 };
 int tuning();
 void set_tuning(int t);

@@ -222,3 +222,20 @@ def test_gelu_table_equals_direct_all_bf16(sd):
     ref = out_small.view(torch.int16)
     assert torch.equal(out_big.view(torch.int16)[:65536], ref)
     assert torch.equal(out_big.view(torch.int16).view(16, 65536), ref.expand(16, 65536))
+
+
+def test_gelu_grad_table_equals_direct_all_bf16(sd):
+    """sd_gelu_backward on large activations reads d GELU/dh from a 16 K-entry
+    table (2^-31 <= |h| < 2^33) and evaluates the rest directly: every bf16
+    h pattern (NaN/Inf included), with random upstream gradients, must give the
+    same output bits as the direct kernel (used below 512 K elements)."""
+    from paper_2411_01238_b200.mlp import gelu_grad
+
+    pats = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.int16).view(torch.bfloat16)
+    h = pats.repeat(16)                            # 1 M elements: table path
+    g = torch.randn(h.numel(), device="cuda", generator=torch.Generator(device="cuda").manual_seed(1)).to(
+        torch.bfloat16)
+    out_big = gelu_grad(h, g)
+    parts = [gelu_grad(h[i:i + 32768].clone(), g[i:i + 32768].clone()) for i in range(0, h.numel(), 32768)]
+    torch.cuda.synchronize()
+    assert torch.equal(out_big.view(torch.int16), torch.cat(parts).view(torch.int16))
