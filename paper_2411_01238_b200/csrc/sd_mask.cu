@@ -95,7 +95,7 @@ __device__ __forceinline__ void wait_workspace_free(const PlanArgs& a) {
                 fb = 1;
                 break;
             }
-            __nanosleep(256);
+            __nanosleep(32);
         }
         fallback = fb;
     }
