@@ -37,6 +37,14 @@
 // problem 1) when the producer nears the end of its current unit, decodes them
 // (list lookups) and hands the decoded unit to the producer, MMA and epilogue
 // roles through a shared-memory ring; zero-work units skip TMEM.
+//
+// Launch overlap (PDL): every CTA triggers its dependents right after its
+// griddepcontrol.wait, which a plan's backward skips when it directly follows
+// the plan's forward (LaunchArgs.no_wait: it reads nothing the forward writes).
+// Mask lists are only read by the scheduler (ld.global.cg, staged in smem): the
+// CTA that decodes the launch's last unit releases the mask workspace for the
+// whole grid (LaunchArgs.release), so the next mask generation can overwrite
+// it while the grid's last units still compute.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
