@@ -634,6 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // counter increment), whatever the CTAs still have to compute
             if (L.release_all && prob >= 0 && lane == 0 &&
                 atomicAdd(L.sched + 2, 1u) == static_cast<unsigned int>(num_units) - 1u) {
+#ifdef SD_TRACE
+                g_sd_timeline[(L.trace_id & 255) * 4 + 3] = gtimer();  // mask workspaces released
+#endif
                 for (int r = 0; r < 2; ++r) {
                     if (L.release[r]) {
                         __threadfence();

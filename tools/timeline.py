@@ -61,6 +61,9 @@ for it in range(4):
             wait = (f" last-past-wait {(lw - t0) / 1e3:7.1f}" if lw else "") + (f" order {(od - t0) / 1e3:7.1f}" if od else "")
         else:
             wait = "" if wt == 0xFFFFFFFFFFFFFFFF else f" past-wait {(wt - t0) / 1e3:7.1f}"
+            rl = int(g[4 * (lid & 255) + 3])
+            if rl and rl != 0xFFFFFFFFFFFFFFFF:
+                wait += f" released {(rl - t0) / 1e3:7.1f}"
         gap = "" if prev_end is None else f" (gap from prev end {(st - prev_end) / 1e3:+.1f})"
         print(f"   {name:5s} #{lid}: start {(st - t0) / 1e3:7.1f}{wait} end {(en - t0) / 1e3:7.1f}  dur {(en - st) / 1e3:6.1f} us{gap}")
         prev_end = en
