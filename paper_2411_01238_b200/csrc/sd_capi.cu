@@ -950,13 +950,15 @@ int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         launch_gemm(plan->dense_fwd, as_stream(stream));
+        plan->fwd_mark = sd_launch_count();
+        plan->fwd_stream = as_stream(stream);
     });
 }
 
 int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), false);
+        fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), take_no_wait(plan, as_stream(stream)));
     });
 }
 

@@ -900,8 +900,12 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
                     (a.rows_out / 256) * (a.cols_out / 256) >= num_sms() / 2;
         }
         if (dense) {
+            // the problems of one call are independent: the second launch needs
+            // nothing from the first (and the first's own wait, or its caller's
+            // no_wait guarantee, covers everything before), so it never waits
             for (int i = 0; i < n; ++i)
-                launch_gemm2(calls[i]->ta, calls[i]->tb, calls[i]->tout, calls[i]->args, nullptr, nullptr, 0, s);
+                launch_gemm2(calls[i]->ta, calls[i]->tb, calls[i]->tout, calls[i]->args, nullptr, nullptr, 0, s,
+                             i == 0 ? no_wait : true);
             return;
         }
     }

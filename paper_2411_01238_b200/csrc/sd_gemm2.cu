@@ -87,6 +87,7 @@ struct Pair2Args {
     const int32_t* pair_cnt;   // [n_pair_rows]
     const int32_t* pair_idx;   // [n_pair_rows][list_stride]: (block << 2) | owner_mask(bit0 = row 2i, bit1 = 2i+1)
     int pair_stride;
+    int no_wait;  // skip griddepcontrol.wait (see launch_gemms)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    ptx::pdl_wait();
+    if (!P.no_wait) ptx::pdl_wait();
     ptx::pdl_launch_dependents();
 
     // static schedule over pair units, heaviest pair rows first (pair rows are
@@ -335,7 +336,8 @@ bool gemm2_supported(const GemmArgs& a) {
 }
 
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
-                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s) {
+                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
+                  bool no_wait) {
     static bool configured = false;
     if (!configured) {
         check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2),
@@ -350,6 +352,7 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     P.pair_cnt = pair_cnt;
     P.pair_idx = pair_idx;
     P.pair_stride = pair_stride;
+    P.no_wait = no_wait && !(tuning() & kTuneNoEarlyBackward) ? 1 : 0;
     const int units = P.n_pair_rows * P.n_col_tiles;
     int clusters = std::min(units, num_sms() / 2);
     if (clusters <= 0) return;

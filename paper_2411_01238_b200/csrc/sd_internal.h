@@ -141,7 +141,8 @@ inline void launch_gemm(const GemmCall& c, cudaStream_t s, bool no_wait = false)
 // launch is dense and has at least one wave of pair tiles.
 bool gemm2_supported(const GemmArgs& a);
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
-                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s);
+                  const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
+                  bool no_wait = false);
 
 // 2D row-major tensor map: `inner` contiguous elements, `outer` rows, 128B swizzle.
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,

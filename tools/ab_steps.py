@@ -30,11 +30,18 @@ for i in range(3):
     plans.append(sd.LayerPlan(x, w, dy, P))
 
 
+DENSE = os.environ.get("DENSE") == "1"  # time the dense step (dense_forward + dense_backward) instead
+
+
 def steps(n, seed0):
     for i in range(n):
         pl = plans[i % 3]
-        pl.forward(seed0 + i)
-        pl.backward()
+        if DENSE:
+            pl.dense_forward()
+            pl.dense_backward()
+        else:
+            pl.forward(seed0 + i)
+            pl.backward()
 
 
 t_end = time.time() + 1.5
@@ -57,4 +64,4 @@ for r in range(rounds):
 lib.sd_set_tuning(0)
 for v in variants:
     xs = sorted(res[v])
-    print(f"S={S} p={P} tuning {v:4d}: {xs[len(xs) // 2] * 1e3:7.1f} us/step (min {xs[0] * 1e3:6.1f})", flush=True)
+    print(f"S={S} p={P} {'dense' if DENSE else 'sparse'} tuning {v:4d}: {xs[len(xs) // 2] * 1e3:7.1f} us/step (min {xs[0] * 1e3:6.1f})", flush=True)
