@@ -427,14 +427,18 @@ def main():
                   flush=True)
         return
 
-    # ---- dense baseline (same kernel, no mask) and cuBLAS for context
-    ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup)
+    # ---- dense baseline (same kernel, no mask) and cuBLAS for context. Each
+    # configuration is timed in its own steady state: under the power cap the
+    # SM clock settles over ~1 s and differs by workload (a 0.3 s pre-roll left
+    # the denominator and the sweep points up to ~10% apart in clock state)
+    settle = max(args.preroll, 1.5 if args.preroll > 0 else 0.0)
+    ms_dense = time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle)
     # the same dense step on the 1-CTA tile machinery the masked GEMMs use
     # (tuning 16: no 2-CTA kernel) — the like-for-like (1-p) reference
     _lib_t = sd.load_library()
     _lib_t.sd_set_tuning(16)
     try:
-        ms_dense_1cta = time_steps(dense_step_fn(), args.steps, args.warmup)
+        ms_dense_1cta = time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle)
     finally:
         _lib_t.sd_set_tuning(0)
     ms_torch = time_steps(torch_step, args.steps, args.warmup)
@@ -516,7 +520,7 @@ def main():
     sweep = []
     if not args.no_sweep:
         for p in SWEEP_P:
-            msp = time_steps(sparse_step_fn(p), max(5, args.steps // 2), 3)
+            msp = time_steps(sparse_step_fn(p), max(5, args.steps // 2), 3, preroll_s=settle)
             pl = plan_for(p)
             kp = pl.mask.keep_count() / pl.mask.total_blocks()
             sweep.append({
@@ -543,7 +547,7 @@ def main():
                 pl8.forward(seed=sd.effective_seed(0, i, 0))
                 pl8.backward()
 
-            ms8 = time_steps(st8, max(5, args.steps // 2), 3)
+            ms8 = time_steps(st8, max(5, args.steps // 2), 3, preroll_s=settle)
             k8 = pl8.mask.keep_count() / pl8.mask.total_blocks()
             t8[f"p{p8}"] = {"ms_per_step": ms8, "keep": k8,
                             "dense_equiv_tflops": 3 * 2 * S8 ** 3 / (ms8 * 1e-3) / 1e12,
@@ -553,7 +557,7 @@ def main():
                     pl8.dense_forward()
                     pl8.dense_backward()
 
-                msd8 = time_steps(dn8, max(5, args.steps // 2), 3)
+                msd8 = time_steps(dn8, max(5, args.steps // 2), 3, preroll_s=settle)
                 t8["dense_ms_per_step"] = msd8
                 t8["dense_tflops"] = 3 * 2 * S8 ** 3 / (msd8 * 1e-3) / 1e12
                 t8["speedup_vs_dense_p0.5"] = msd8 / ms8
