@@ -683,9 +683,28 @@ struct sd_layer_plan {
     uint64_t fwd_mark = ~0ull;
     cudaStream_t fwd_stream = nullptr;
     bool early_backward = true;  // false when buffers alias (sd_layer_plan_create)
+    // low p: dX as the 2-CTA dense GEMM with dropped output blocks written as
+    // +0.0 (every kept block is reduced over the same 64-deep stages in the same
+    // order as in the sdd kernel: bit-identical)
+    sd::GemmCall dx_masked;
+    bool dx_masked_ok = false;
 };
 
 namespace {
+constexpr double kMaskedDenseMaxP = 0.3;
+
+// Measured (tools/ab_steps.py, profiles/r01_masked_dx_ab.txt): at 4096^3 the
+// split backward gains 1-2% at p <= 0.2 and loses 3% at p = 0.3 (the fused
+// dW+dX queue's shared tail is worth more there); at 8192^3, -12% at p = 0.1
+// and -5% at p = 0.3. So p <= 0.2, or p <= 0.3 with at least four waves of
+// 256x256 pair tiles.
+bool use_masked_dx(const sd_layer_plan* plan) {
+    if (!plan->dx_masked_ok || (sd::tuning() & sd::kTuneNoMaskedDense) || !sd::gemm2_routed(plan->dx_masked.args))
+        return false;
+    const int64_t tiles = static_cast<int64_t>(plan->dx_masked.args.rows_out / 256) * (plan->dx_masked.args.cols_out / 256);
+    return plan->p <= 0.2 || tiles >= 4 * static_cast<int64_t>(sd::num_sms());
+}
+
 // The backward reads X, W, dY and the mask lists and writes dX, dW; the forward
 // reads X, W and the lists and writes Y. So the first backward launch right
 // after the plan's forward (no launch of ours in between, same stream) needs
@@ -857,6 +876,18 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
         tmp.x = x;
         tmp.m = m, tmp.n = n, tmp.k = k;
+        // Masked dense dX: sdd over the kept fraction (1 - p) of the blocks on
+        // 1-CTA tiles costs ~1.2-1.4x the 2-CTA kernel's time per MAC
+        // (profiles/r01_masked_dx_ab.txt), so below p = kMaskedDenseMaxP the
+        // full dense product with zeroed dropped blocks is faster.
+        tmp.dx_masked = tmp.dense_dx;
+        tmp.dx_masked.args.scale = s;
+        tmp.dx_masked.args.flags |= kFlagOutMask;
+        tmp.dx_masked.args.words = mask->words;
+        tmp.dx_masked.args.mask_cols = mask->block_cols;
+        tmp.dx_masked.release = mask_release_counter(mask);
+        tmp.dx_masked_ok = p <= kMaskedDenseMaxP && mask->m_blk == 128 && mask->k_blk == 128 &&
+                           gemm2_supported(tmp.dx_masked.args);
         // the early backward relies on the forward writing nothing the backward
         // touches: with Y overlapping X, W, dY, dX or dW, or the mask workspace
         // overlapping any buffer, every backward waits for the forward grid
@@ -933,7 +964,8 @@ int sd_layer_plan_backward_dw_part(sd_layer_plan* plan, int32_t part, int32_t np
 int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        launch_gemm(plan->dx, as_stream(stream), take_no_wait(plan, as_stream(stream)));
+        launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, as_stream(stream),
+                    take_no_wait(plan, as_stream(stream)));
     });
 }
 
@@ -941,8 +973,16 @@ int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         const bool nw = take_no_wait(plan, as_stream(stream));
-        if (plan_dense(plan)) fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), nw);
-        else fused_backward(plan->dx, plan->dw, as_stream(stream), nw);
+        if (plan_dense(plan)) {
+            fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), nw);
+        } else if (use_masked_dx(plan)) {
+            // dW on the 1-CTA kernel, dX on the 2-CTA kernel: independent
+            // launches, the second never waits for the first
+            launch_gemm(plan->dw, as_stream(stream), nw);
+            launch_gemm(plan->dx_masked, as_stream(stream), true);
+        } else {
+            fused_backward(plan->dx, plan->dw, as_stream(stream), nw);
+        }
     });
 }
 

@@ -892,22 +892,20 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     }
     // dense problems go to the 2-CTA kernel (half the per-SM operand traffic
     // per MAC: tools/gemm2_check.py, +10-25% over this kernel at 4096-8192)
-    if (!(g_tuning & kTuneNoGemm2)) {
+    {
         bool dense = true;
-        for (int i = 0; i < n; ++i) {
-            const GemmArgs& a = calls[i]->args;
-            dense = dense && a.list_cnt == nullptr && a.counters == nullptr && gemm2_supported(a) &&
-                    (a.rows_out / 256) * (a.cols_out / 256) >= num_sms() / 2;
-        }
+        for (int i = 0; i < n; ++i) dense = dense && gemm2_routed(calls[i]->args);
         if (dense) {
             // the problems of one call are independent: the second launch needs
             // nothing from the first (and the first's own wait, or its caller's
             // no_wait guarantee, covers everything before), so it never waits
             for (int i = 0; i < n; ++i)
                 launch_gemm2(calls[i]->ta, calls[i]->tb, calls[i]->tout, calls[i]->args, nullptr, nullptr, 0, s,
-                             i == 0 ? no_wait : true);
+                             i == 0 ? no_wait : true, calls[i]->release);
             return;
         }
+        for (int i = 0; i < n; ++i)
+            if (calls[i]->args.flags & kFlagOutMask) fail(SD_ERUNTIME, "masked dense GEMM not routable to the 2-CTA kernel");
     }
     TensorMaps tms;
     LaunchArgs L;

@@ -88,6 +88,7 @@ struct Pair2Args {
     const int32_t* pair_idx;   // [n_pair_rows][list_stride]: (block << 2) | owner_mask(bit0 = row 2i, bit1 = 2i+1)
     int pair_stride;
     int no_wait;  // skip griddepcontrol.wait (see launch_gemms)
+    unsigned int* release;  // mask workspace read (kFlagOutMask words): +1 per CTA at exit
 };
 
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
@@ -284,6 +285,14 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 ptx::tmem_ld_32x32b_x32(taddr, v);
                 if (!f32) ptx::tmem_ld_32x32b_x32(taddr + 32, v + 32);
                 ptx::tmem_ld_wait();
+                if (a.flags & kFlagOutMask) {
+                    // dropped 128x128 output block (dX = s (dY W^T) (.) m): exact +0.0
+                    const int64_t bit = static_cast<int64_t>(row_first / 128) * a.mask_cols + (ct * kTile + c * chunk) / 128;
+                    if (!((__ldcg(a.words + (bit >> 6)) >> (bit & 63)) & 1ull)) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) v[j] = 0u;
+                    }
+                }
                 if (c == nchunks - 1) {
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -326,9 +335,18 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+    if (P.release && threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(P.release, 1u);
+    }
 }
 
 }  // namespace
+
+bool gemm2_routed(const GemmArgs& a) {
+    return !(tuning() & kTuneNoGemm2) && a.list_cnt == nullptr && a.counters == nullptr && gemm2_supported(a) &&
+           (a.rows_out / 256) * (a.cols_out / 256) >= num_sms() / 2;
+}
 
 bool gemm2_supported(const GemmArgs& a) {
     return !(a.flags & (kFlagSDD | kFlagReduce)) && a.rows_out % 256 == 0 && a.cols_out % 256 == 0 &&
@@ -337,7 +355,7 @@ bool gemm2_supported(const GemmArgs& a) {
 
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
-                  bool no_wait) {
+                  bool no_wait, unsigned int* release) {
     static bool configured = false;
     if (!configured) {
         check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2),
@@ -353,6 +371,7 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     P.pair_idx = pair_idx;
     P.pair_stride = pair_stride;
     P.no_wait = no_wait && !(tuning() & kTuneNoEarlyBackward) ? 1 : 0;
+    P.release = release;
     const int units = P.n_pair_rows * P.n_col_tiles;
     int clusters = std::min(units, num_sms() / 2);
     if (clusters <= 0) return;
@@ -368,6 +387,7 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel, ta, tb, tout, P), "sd_gemm2_kernel launch");
     note_launch();
+    if (release) mask_note_readers(release, static_cast<int>(cfg.gridDim.x), s);
     // this kernel does not release mask workspaces: a following generation
     // into one it reads waits for the whole grid
     for (const void* q : {static_cast<const void*>(pair_cnt), static_cast<const void*>(pair_idx),

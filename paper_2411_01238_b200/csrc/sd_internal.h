@@ -60,6 +60,8 @@ enum GemmFlags : uint32_t {
     kFlagSDD = 4u,  // output-block skipping (sdd) instead of reduction-block skipping (dsd)
     kFlagF32 = 8u,  // fp32 output, else bf16
     kFlagReduce = 16u,  // split-K: the epilogue reduce-adds into a pre-zeroed fp32 output
+    kFlagOutMask = 32u,  // 2-CTA dense only: output blocks dropped in `words` (128x128, mask_cols
+                         // per row) are written as +0.0 (dX at low p: masked dense, see sd_capi.cu)
 };
 
 struct GemmArgs {
@@ -119,6 +121,7 @@ enum TuneFlags : int {
     kTuneNoEarlyBackward = 128,  // a plan's backward waits for its forward grid (griddepcontrol.wait)
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
     kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
+    kTuneNoMaskedDense = 1024,   // low-p dX stays on the sdd kernel instead of the masked 2-CTA dense GEMM
 };
 int tuning();
 void set_tuning(int t);
@@ -142,7 +145,9 @@ inline void launch_gemm(const GemmCall& c, cudaStream_t s, bool no_wait = false)
 bool gemm2_supported(const GemmArgs& a);
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
-                  bool no_wait = false);
+                  bool no_wait = false, unsigned int* release = nullptr);
+// launch_gemms sends a problem to the 2-CTA kernel when this holds
+bool gemm2_routed(const GemmArgs& a);
 
 // 2D row-major tensor map: `inner` contiguous elements, `outer` rows, 128B swizzle.
 CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,

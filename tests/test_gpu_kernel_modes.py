@@ -239,3 +239,38 @@ def test_gelu_grad_table_equals_direct_all_bf16(sd):
     parts = [gelu_grad(h[i:i + 32768].clone(), g[i:i + 32768].clone()) for i in range(0, h.numel(), 32768)]
     torch.cuda.synchronize()
     assert torch.equal(out_big.view(torch.int16), torch.cat(parts).view(torch.int16))
+
+
+@pytest.mark.parametrize("p", [0.1, 0.2, 0.3])
+@pytest.mark.parametrize("entry", ["fused", "dx_only"])
+def test_masked_dense_dx_equals_sdd_bitwise(sd, oracle, p, entry):
+    """At low p the plan computes dX as the 2-CTA dense GEMM with dropped output
+    blocks written as +0.0 (tuning bit 1024 keeps the sdd kernel): same bits,
+    dropped blocks exactly +0.0."""
+    lib = sd.load_library()
+    M = N = K = 4096
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    outs = []
+    try:
+        for bits in (0, 1024):
+            lib.sd_set_tuning(bits)
+            plan = sd.LayerPlan(x, w, dy, p)
+            plan.forward(11)
+            if entry == "fused":
+                plan.backward()
+            else:
+                plan.backward_dx()
+                plan.backward_dw()
+            torch.cuda.synchronize()
+            outs.append((plan.dx.clone(), plan.dw.clone(), plan.mask.words()))
+    finally:
+        lib.sd_set_tuning(0)
+    (dx0, dw0, m0), (dx1, dw1, m1) = outs
+    assert m0 == m1
+    assert torch.equal(dx0.view(torch.int16), dx1.view(torch.int16))
+    assert torch.equal(dw0, dw1)
+    kept = np.array(m0, dtype=np.uint64)
+    bits = np.unpackbits(kept.view(np.uint8), bitorder="little")[: 32 * 32].reshape(32, 32)
+    blocks = dx0.view(32, 128, 32, 128).permute(0, 2, 1, 3).reshape(32, 32, -1)
+    dropped = torch.from_numpy(bits == 0).cuda()
+    assert (blocks[dropped].view(torch.int16) == 0).all()
