@@ -1,6 +1,6 @@
 """Union-mode 2-CTA dsd vs the 1-CTA kernels (dev tool): pair lists built on the
 host from the mask; checks bitwise equality with the 1-CTA forward/dW and times
-both.  python tools/union_probe.py SIZE P..."""
+both.  python tools/union_probe.py SIZE|M,N,K P..."""
 import ctypes
 import os
 import sys
@@ -16,8 +16,8 @@ lib.sd_dev_dsd_pairs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void
                                  ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                  ctypes.c_void_p, ctypes.c_int32, ctypes.c_float, ctypes.c_void_p]
 lib.sd_last_error.restype = ctypes.c_char_p
-S = int(sys.argv[1])
-M = N = K = S
+S = sys.argv[1]  # SIZE or M,N,K
+M, N, K = (int(v) for v in S.split(",")) if "," in S else (int(S),) * 3
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 w = torch.randn(K, N, device="cuda").to(torch.bfloat16)
 dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
