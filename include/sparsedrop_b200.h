@@ -236,7 +236,11 @@ SD_API uint64_t sd_launch_count(void);
  *    forward's last wave frees; it reads nothing the forward writes),
  * 256 mask generation waits for the whole preceding grid (default, for a
  *    workspace bound by sd_mask_bind: only for the GEMM CTAs still reading its
- *    previous lists, which release it when their last list read is done).
+ *    previous lists, which release it when their last list read is done),
+ * 512 GELU' evaluated per element instead of from the shared-memory table,
+ * 1024 a low-p plan's dX stays on the sdd kernel (default: p <= 0.2, or <= 0.3
+ *    on large problems, computes dX as the 2-CTA dense GEMM with dropped output
+ *    blocks written as +0.0; bit-identical).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 
