@@ -867,11 +867,18 @@ static bool wide_units(const GemmCall* const* calls, int n) {
     if (g_tuning & kTuneNarrow) return false;
     if (g_tuning & kTuneWide) return true;
     // fewer wide units than SMs: the launch is latency-bound and twice as many
-    // narrow units finish sooner (1024^3 layer step -6.5%, 2048^3 -2%)
+    // narrow units finish sooner (1024^3 layer step -6.5%, 2048^3 -2%) —
+    // unless a problem will be split along its long reduction instead (fp32
+    // dsd: the MLP's dW), which fills the SMs either way
     int64_t wide_count = 0;
-    for (int i = 0; i < n; ++i)
-        wide_count += static_cast<int64_t>(calls[i]->args.n_row_tiles) * ((calls[i]->args.cols_out + 2 * kBN - 1) / (2 * kBN));
-    if (wide_count < num_sms()) return false;
+    bool splittable = false;
+    for (int i = 0; i < n; ++i) {
+        const GemmArgs& a = calls[i]->args;
+        wide_count += static_cast<int64_t>(a.n_row_tiles) * ((a.cols_out + 2 * kBN - 1) / (2 * kBN));
+        splittable = splittable || (!(g_tuning & kTuneNoSplitK) && !(a.flags & kFlagSDD) && (a.flags & kFlagF32) &&
+                                    a.red / kBK >= 64);
+    }
+    if (!splittable && wide_count < num_sms()) return false;
     for (int i = 0; i < n; ++i) {
         const GemmArgs& a = calls[i]->args;
         if ((a.flags & kFlagSDD) || a.cols_out <= kBN) return false;
