@@ -621,8 +621,10 @@ def main():
                            "dense_1cta_ms_per_step: the same dense step on the 1-CTA tiles the masked GEMMs use"),
             "isolated_ms_per_step": ms_isolated,
             "timing": (f"{n_sets} rotating input sets ({n_sets * set_bytes / 2**20:.0f} MiB > L2), steps back-to-back, "
-                       "one CUDA-event pair around the K timed steps; isolated_ms_per_step: one step at a time "
-                       "with a 512 MiB L2 flush before each, per-step events (includes launch latency)"),
+                       "one CUDA-event pair around the K timed steps; every leg (headline, dense, sweep points, t8) "
+                       "after 1.5 s of its own sustained load (power-capped steady state); isolated_ms_per_step: "
+                       "one step at a time with a 512 MiB L2 flush before each, per-step events (includes launch "
+                       "latency)"),
             "torch_cublas_dense_ms_per_step": ms_torch,
             "gpu_launches": gpu_launches,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
