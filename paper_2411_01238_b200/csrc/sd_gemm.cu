@@ -99,6 +99,9 @@ namespace {
 #ifndef SD_CLAIM_LEAD_W
 #define SD_CLAIM_LEAD_W 4
 #endif
+#ifndef SD_WEPIBUFS
+#define SD_WEPIBUFS 2  // wide: store boxes per epilogue warp (1 frees 16 KB for a 5th B slot)
+#endif
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB: one A slot (128 rows x 64)
 constexpr int kBBytes = kBN * kBK * 2;  // 32 KB: one B slot (256 columns x 64)
 constexpr int kEpiWarps = 4;
@@ -141,10 +144,11 @@ struct KCfg {
     static constexpr int kSB = WIDE ? SD_WSTAGES_B : SD_STAGES;
     static constexpr int kWidth = WIDE ? 2 * kBN : kBN;
     static constexpr int kClaimLead = WIDE ? SD_CLAIM_LEAD_W : SD_CLAIM_LEAD;
+    static constexpr int kEpiBufs = WIDE ? SD_WEPIBUFS : 2;
     static constexpr int kOffA = 0;
     static constexpr int kOffB = kOffA + kSA * kABytes;
     static constexpr int kOffEpi = kOffB + kSB * kBBytes;
-    static constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+    static constexpr int kOffBar = kOffEpi + kEpiWarps * kEpiBufs * kEpiBufBytes;
     // full[kSB] empty[kSB] aempty[kSA] tfull[2] tempty[2] sfull[D] sempty[D] claim
     static constexpr int kNumBars = 2 * kSB + kSA + 4 + 2 * kSchedDepth + 1;
     static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
@@ -347,7 +351,10 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
             }
         }
         // staging buffer bi must no longer be read by the TMA store issued 2 chunks ago
-        if (lane == 0) ptx::bulk_wait_group_read<1>();
+        if (lane == 0) {
+            if constexpr (KCfg<WIDE>::kEpiBufs == 2) ptx::bulk_wait_group_read<1>();
+            else ptx::bulk_wait_group_read<0>();
+        }
         __syncwarp();
         const uint32_t row_addr = ebuf_addr + bi * kEpiBufBytes + lane * 128;
 #pragma unroll
@@ -384,7 +391,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
                 ptx::tma_store_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
             ptx::bulk_commit_group();
         }
-        bi ^= 1;
+        if constexpr (KCfg<WIDE>::kEpiBufs == 2) bi ^= 1;
     }
 }
 
@@ -773,8 +780,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ===================== epilogue =====================
         const uint32_t q = warp & 3;  // TMEM lane quarter == output row quarter
-        uint8_t* ebuf = smem + C::kOffEpi + q * 2 * kEpiBufBytes;
-        const uint32_t ebuf_addr = sbase + C::kOffEpi + q * 2 * kEpiBufBytes;
+        uint8_t* ebuf = smem + C::kOffEpi + q * C::kEpiBufs * kEpiBufBytes;
+        const uint32_t ebuf_addr = sbase + C::kOffEpi + q * C::kEpiBufs * kEpiBufBytes;
         uint32_t bi = 0;
         uint32_t acc_iter = 0;
         int sslot = 0;
