@@ -438,8 +438,9 @@ def backward(layer: LinearLayer, ctx: LayerContext, dy: torch.Tensor, stream=Non
 
 class LayerPlan:
     """A bound sparsedrop layer (C-ABI sd_layer_plan): buffers and tensor maps are
-    fixed at construction, each step is 2 (forward) + 2 (backward) kernel
-    launches with no host-side work — the runtime object a training loop keeps
+    fixed at construction, each step is 2 (forward) + 1 (backward; 2 at p <= 0.2,
+    where dX runs on the masked 2-CTA dense kernel) kernel launches with no
+    host-side work — the runtime object a training loop keeps
     per layer. Row shards pass `row_block_offset` (global block row of local row 0).
 
     forward(seed)   : mask = sample_mask(seed) ; y = s (x (.) m) w
