@@ -152,6 +152,30 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         ct = rem / rows_in_group;
         prow = g * G + (rem - ct * rows_in_group);
     };
+
+    // kFlagOutMask: this CTA's keep bits (its 128-row block x the tile's two
+    // 128-column blocks) for every unit it will run, read once up front, so the
+    // mask workspace is released now instead of at exit and the next mask
+    // generation overlaps this grid (more than kMaxOwnUnits units: at exit)
+    constexpr int kMaxOwnUnits = 512;
+    __shared__ uint8_t own_bits[kMaxOwnUnits];
+    const int own_units = (num_units - cluster_id + n_clusters - 1) / n_clusters;
+    const bool bits_up_front = (a.flags & kFlagOutMask) && own_units <= kMaxOwnUnits;
+    if (bits_up_front) {
+        for (int k = threadIdx.x; k < own_units; k += kThreads) {
+            int prow, ct;
+            decode(cluster_id + k * n_clusters, prow, ct);
+            const int64_t bit = static_cast<int64_t>(2 * prow + static_cast<int>(rank)) * a.mask_cols + 2 * ct;
+            const uint64_t w0 = __ldcg(a.words + (bit >> 6));
+            const uint64_t w1 = __ldcg(a.words + ((bit + 1) >> 6));
+            own_bits[k] = static_cast<uint8_t>(((w0 >> (bit & 63)) & 1ull) | (((w1 >> ((bit + 1) & 63)) & 1ull) << 1));
+        }
+        __syncthreads();
+        if (P.release && threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(P.release, 1u);
+        }
+    }
     auto unit_stages = [&](int prow) -> int {
         if (unioned) return __ldg(P.pair_cnt + prow) * (a.red_blk / kBK);
         return a.red / kBK;
@@ -287,8 +311,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 ptx::tmem_ld_wait();
                 if (a.flags & kFlagOutMask) {
                     // dropped 128x128 output block (dX = s (dY W^T) (.) m): exact +0.0
-                    const int64_t bit = static_cast<int64_t>(row_first / 128) * a.mask_cols + (ct * kTile + c * chunk) / 128;
-                    if (!((__ldcg(a.words + (bit >> 6)) >> (bit & 63)) & 1ull)) {
+                    const int cb = (c * chunk) / 128;  // column block within the tile
+                    bool kept;
+                    if (bits_up_front) {
+                        kept = (own_bits[(u - cluster_id) / n_clusters] >> cb) & 1u;
+                    } else {
+                        const int64_t bit = static_cast<int64_t>(row_first / 128) * a.mask_cols + 2 * ct + cb;
+                        kept = (__ldcg(a.words + (bit >> 6)) >> (bit & 63)) & 1ull;
+                    }
+                    if (!kept) {
 #pragma unroll
                         for (int j = 0; j < 64; ++j) v[j] = 0u;
                     }
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
-    if (P.release && threadIdx.x == 0) {
+    if (P.release && !bits_up_front && threadIdx.x == 0) {
         __threadfence();
         atomicAdd(P.release, 1u);
     }
