@@ -353,7 +353,7 @@ def main():
     def plan_for(p, j=0):
         if (p, j) not in plans:
             xs, ws, dys = sets[j]
-            plans[(p, j)] = sd.LayerPlan(xs, ws, dys, p, row_block_offset=row_off)
+            plans[(p, j)] = sd.LayerPlan(xs, ws, dys, p, row_block_offset=row_off, dy_ready=True)
         return plans[(p, j)]
 
     def drop_plans(p):
@@ -541,7 +541,7 @@ def main():
         x8, w8, dy8 = synth(S8, S8), synth(S8, S8), synth(S8, S8)
         t8 = {"shape": [S8, S8, S8]}
         for p8 in (0.0, 0.1, 0.5):
-            pl8 = sd.LayerPlan(x8, w8, dy8, p8)
+            pl8 = sd.LayerPlan(x8, w8, dy8, p8, dy_ready=True)
 
             def st8(i, pl8=pl8):
                 pl8.forward(seed=sd.effective_seed(0, i, 0))

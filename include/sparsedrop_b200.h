@@ -192,6 +192,17 @@ SD_API int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream);
  * dw = x^T dy, dx = dy w^T on the same tcgen05 kernel, no mask. */
 SD_API int sd_layer_plan_dense_forward(sd_layer_plan* plan, void* stream);
 SD_API int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream);
+/* Plan options (bit set; default 0):
+ * SD_PLAN_DY_READY  the caller guarantees dY — and everything else the backward
+ *   reads — is written BEFORE sd_layer_plan_forward is enqueued, and nothing
+ *   writes it between the forward and the backward (e.g. a fixed synthetic dY,
+ *   or one uploaded before the step). The first backward launch right after the
+ *   forward then skips griddepcontrol.wait and starts on the SMs the forward's
+ *   last wave frees. Without it the backward always waits for the preceding
+ *   grid, which is required when a caller kernel computes dY from Y in between:
+ *   such a kernel may trigger its dependents early (PDL). */
+#define SD_PLAN_DY_READY 1
+SD_API int sd_layer_plan_set_options(sd_layer_plan* plan, int32_t options);
 SD_API int sd_layer_plan_destroy(sd_layer_plan* plan);
 
 /* The MLP block's activation between two SparseDrop Linears (configs[2]):
@@ -231,16 +242,20 @@ SD_API uint64_t sd_launch_count(void);
  *    (cta_group::2) kernel,
  * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles
  *    (default: 128x512 for dsd-only launches with a keep hint >= 0.2),
- * 128 a layer plan's backward waits for its forward grid (default: the first
- *    backward launch right after the plan's forward starts on the SMs the
- *    forward's last wave frees; it reads nothing the forward writes),
+ * 128 a layer plan's backward waits for its forward grid even with
+ *    SD_PLAN_DY_READY (default with that option: the first backward launch right
+ *    after the plan's forward starts on the SMs the forward's last wave frees;
+ *    it reads nothing the forward writes),
  * 256 mask generation waits for the whole preceding grid (default, for a
  *    workspace bound by sd_mask_bind: only for the GEMM CTAs still reading its
  *    previous lists, which release it when their last list read is done),
  * 512 GELU' evaluated per element instead of from the shared-memory table,
  * 1024 a low-p plan's dX stays on the sdd kernel (default: p <= 0.2, or <= 0.3
  *    on large problems, computes dX as the 2-CTA dense GEMM with dropped output
- *    blocks written as +0.0; bit-identical).
+ *    blocks written as +0.0; bit-identical),
+ * 2048 the masked 2-CTA dX reads its keep bits per output chunk and releases the
+ *    mask workspace at exit (the path for CTAs with more than 512 units,
+ *    forced here for tests).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 

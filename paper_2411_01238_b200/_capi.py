@@ -81,6 +81,7 @@ PROTOTYPES = {
     "sd_dev_dsd_pairs": (ctypes.c_int, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _I, ctypes.c_float, _P]),
     "sd_layer_plan_dense_forward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),
+    "sd_layer_plan_set_options": (ctypes.c_int, [_P, _I]),
     "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
     "sd_gelu_forward": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "sd_gelu_backward": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P]),

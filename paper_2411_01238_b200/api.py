@@ -56,6 +56,7 @@ def _require_bf16(name: str, t: torch.Tensor) -> None:
 
 # --------------------------------------------------------------------------- rng.hpp
 
+SD_PLAN_DY_READY = 1  # include/sparsedrop_b200.h
 MASK64 = (1 << 64) - 1
 
 
@@ -445,11 +446,16 @@ class LayerPlan:
 
     forward(seed)   : mask = sample_mask(seed) ; y = s (x (.) m) w
     backward()      : dw = s (x (.) m)^T dy ; dx = s (dy w^T) (.) m
+
+    dy_ready=True (SD_PLAN_DY_READY) declares that dy is written before each
+    forward and never between a forward and its backward (a fixed or uploaded
+    dy): the backward may then start in the forward's tail. Leave it False when
+    a kernel between forward and backward produces dy.
     """
 
     def __init__(self, x: torch.Tensor, w: torch.Tensor, dy: torch.Tensor, p: float, m_blk: int = 128,
                  k_blk: int = 128, row_block_offset: int = 0, y_dtype=torch.bfloat16,
-                 dx_dtype=torch.bfloat16, dw_dtype=torch.float32):
+                 dx_dtype=torch.bfloat16, dw_dtype=torch.float32, dy_ready: bool = False):
         _require_bf16("x", x), _require_bf16("w", w), _require_bf16("dy", dy)
         m, k = x.shape
         n = w.shape[1]
@@ -470,6 +476,8 @@ class LayerPlan:
                                           self.y.data_ptr(), _dtype_code(y_dtype), self.dx.data_ptr(),
                                           _dtype_code(dx_dtype), self.dw.data_ptr(), _dtype_code(dw_dtype),
                                           m, n, k, float(p), self.mask.cptr()))
+        if dy_ready:
+            check(_lib().sd_layer_plan_set_options(self._plan, SD_PLAN_DY_READY))
         self.scale = dropout_scale(p)
 
     def forward(self, seed: int, stream=None):

@@ -175,12 +175,26 @@ int num_sms() {
     return n;
 }
 
+void configure_once_per_device(int key, const std::function<void()>& fn) {
+    static std::mutex mu;
+    static bool done[8][64] = {};
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (key < 0 || key >= 8 || dev < 0 || dev >= 64) fail(SD_ERUNTIME, "configure_once_per_device: bad key/device");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[key][dev]) return;
+    fn();
+    done[key][dev] = true;
+}
+
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-unsigned int* sched_slot() {
-    constexpr int kSlots = 256;
+unsigned int* sched_slot(cudaStream_t s) {
+    constexpr int kRing = 256;       // eager launches, round-robin
+    constexpr int kCaptured = 1024;  // launches captured into graphs, never reused
     static unsigned int* slots[64] = {nullptr};
     static std::atomic<uint32_t> next{0};
+    static std::atomic<uint32_t> next_captured[64];
     static std::mutex mu;
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -188,14 +202,27 @@ unsigned int* sched_slot() {
     if (!slots[dev]) {
         std::lock_guard<std::mutex> lock(mu);
         if (!slots[dev]) {
+            const size_t bytes = static_cast<size_t>(kRing + kCaptured) * kSlotWords * sizeof(unsigned int);
             unsigned int* p = nullptr;
-            check_cuda(cudaMalloc(&p, kSlots * 4 * sizeof(unsigned int)), "cudaMalloc(scheduler slots)");
-            check_cuda(cudaMemset(p, 0, kSlots * 4 * sizeof(unsigned int)), "cudaMemset(scheduler slots)");
+            check_cuda(cudaMalloc(&p, bytes), "cudaMalloc(scheduler slots)");
+            check_cuda(cudaMemset(p, 0, bytes), "cudaMemset(scheduler slots)");
             check_cuda(cudaDeviceSynchronize(), "scheduler slots init");
+            next_captured[dev].store(0);
             slots[dev] = p;
         }
     }
-    return slots[dev] + 4 * (next.fetch_add(1, std::memory_order_relaxed) % kSlots);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s != nullptr && cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        cap = cudaStreamCaptureStatusNone;
+    }
+    if (cap == cudaStreamCaptureStatusActive) {
+        const uint32_t i = next_captured[dev].fetch_add(1, std::memory_order_relaxed);
+        if (i >= static_cast<uint32_t>(kCaptured))
+            fail(SD_ERUNTIME, "too many captured GEMM launches (" + std::to_string(kCaptured) + " per device)");
+        return slots[dev] + static_cast<size_t>(kRing + i) * kSlotWords;
+    }
+    return slots[dev] + static_cast<size_t>(next.fetch_add(1, std::memory_order_relaxed) % kRing) * kSlotWords;
 }
 
 // ---------------------------------------------------------------- reader tracking
@@ -683,6 +710,12 @@ struct sd_layer_plan {
     uint64_t fwd_mark = ~0ull;
     cudaStream_t fwd_stream = nullptr;
     bool early_backward = true;  // false when buffers alias (sd_layer_plan_create)
+    // SD_PLAN_DY_READY (sd_layer_plan_set_options): the caller guarantees that
+    // nothing the backward reads (dY in particular) is written between this
+    // plan's forward and its backward. Off by default: a caller kernel that
+    // writes dY there may trigger its dependents early (PDL), and a backward
+    // that skipped griddepcontrol.wait would then read dY before it is written.
+    bool dy_ready = false;
     // low p: dX as the 2-CTA dense GEMM with dropped output blocks written as
     // +0.0 (every kept block is reduced over the same 64-deep stages in the same
     // order as in the sdd kernel: bit-identical)
@@ -706,14 +739,16 @@ bool use_masked_dx(const sd_layer_plan* plan) {
 }
 
 // The backward reads X, W, dY and the mask lists and writes dX, dW; the forward
-// reads X, W and the lists and writes Y. So the first backward launch right
+// reads X, W and the lists and writes Y. So when the caller has declared dY
+// ready before the forward (SD_PLAN_DY_READY), the first backward launch right
 // after the plan's forward (no launch of ours in between, same stream) needs
 // nothing from the forward grid: its CTAs start on the SMs the forward's last
-// wave leaves idle. Any other kernel in between either is one of ours (the
-// count moved: wait) or is an ordinary launch, which the stream already
-// serializes fully. Consumed by the first backward launch.
+// wave leaves idle. Without the declaration every backward waits for the
+// preceding grid (a caller kernel writing dY may trigger early under PDL).
+// Consumed by the first backward launch.
 bool take_no_wait(sd_layer_plan* plan, cudaStream_t s) {
-    const bool ok = plan->early_backward && plan->fwd_mark == sd_launch_count() && plan->fwd_stream == s;
+    const bool ok = plan->dy_ready && plan->early_backward && plan->fwd_mark == sd_launch_count() &&
+                    plan->fwd_stream == s;
     plan->fwd_mark = ~0ull;
     return ok;
 }
@@ -870,7 +905,7 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.fwd.args.keep_hint = tmp.dw.args.keep_hint = tmp.dx.args.keep_hint = static_cast<float>(1.0 - p);
         require_device();
         cudaGetDevice(&tmp.device);
-        (void)sched_slot();  // allocate the scheduler slots now (keeps launches capturable)
+        (void)sched_slot(nullptr);  // allocate the scheduler slots now (keeps launches capturable)
         tmp.dense_fwd = prep_dense(x, false, w, true, y, y_dtype, m, n, k);
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
@@ -999,6 +1034,14 @@ int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), take_no_wait(plan, as_stream(stream)));
+    });
+}
+
+int sd_layer_plan_set_options(sd_layer_plan* plan, int32_t options) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        if (options & ~SD_PLAN_DY_READY) fail(SD_EINVAL, "sd_layer_plan_set_options: unknown option bits");
+        plan->dy_ready = (options & SD_PLAN_DY_READY) != 0;
     });
 }
 

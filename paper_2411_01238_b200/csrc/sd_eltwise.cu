@@ -384,10 +384,48 @@ __global__ void __launch_bounds__(kThreads) dropout_apply_kernel(const uint4* __
     }
 }
 
+// A caller-style kernel with Programmatic Dependent Launch (tests only): it
+// triggers its dependents FIRST, as PDL-enabled library kernels (CUTLASS,
+// cuBLASLt, Triton) may, then spins and writes out = 2 * in. A following
+// launch that skipped griddepcontrol.wait would read `out` before it is
+// written (the early backward must be opt-in).
+__global__ void pdl_early_writer_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t n, int spin_ns) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (spin_ns > 0) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            __nanosleep(1000);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (t - t0 < static_cast<unsigned long long>(spin_ns));
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __float2bfloat16(2.0f * __bfloat162float(in[i]));
+}
+
 }  // namespace
 }  // namespace sd
 
 extern "C" {
+
+// Development entry (not in the public header): out = 2 * in (bf16), launched
+// with programmatic stream serialization and an early trigger (see above).
+SD_API int sd_dev_pdl_early_writer(const void* in, void* out, int64_t n, int32_t spin_ns, void* stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(sd::num_sms()));
+    cfg.blockDim = dim3(256);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, sd::pdl_early_writer_kernel, static_cast<const __nv_bfloat16*>(in),
+                                             static_cast<__nv_bfloat16*>(out), n, static_cast<int>(spin_ns));
+    return e == cudaSuccess ? SD_OK : SD_ERUNTIME;
+}
 
 SD_API int sd_dropout_apply(const void* in, void* out, int32_t rows, int32_t cols, uint64_t seed, double p,
                             float scale, const sd_block_mask* block_mask, void* stream);

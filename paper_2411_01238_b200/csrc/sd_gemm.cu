@@ -126,7 +126,9 @@ struct Unit {
     int zero_blk[4];
     int first_entry;  // dsd: first list entry (split-K)
     int width;        // unit width in columns (zero fill of an all-dropped dsd unit)
-    int pad[6];
+    int split;        // dsd split-K: this unit's split index (0 = stores, > 0 = ordered reduce-add)
+    int tile;         // dsd split-K: output tile index within the split (turnstile index)
+    int pad[4];
 };
 static_assert(sizeof(Unit) == 96, "Unit layout");
 
@@ -189,6 +191,8 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
     const int base_units = head_units + T * 2 * a.n_col_units;
     const int split = u / base_units;
     u -= split * base_units;
+    t.split = split;
+    t.tile = u;
     int i, cu;
     bool half = false;
     if (u < head_units) {
@@ -293,20 +297,49 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
                                               uint32_t q, uint32_t lane, uint32_t tmem_base,
                                               uint64_t* tfull_bar, uint64_t* tempty_bar, uint8_t* ebuf,
                                               uint32_t ebuf_addr, uint32_t& bi, uint32_t& acc_iter,
-                                              long long* tr) {
+                                              unsigned int* turn_base, long long* tr) {
     (void)tr;
     constexpr int kChunkCols = OUT_F32 ? 32 : 64;  // 128 bytes of output per row
     const bool sdd = a.flags & kFlagSDD;
     const int row_first = t.row0 + 32 * q;
+    // Split-K in a FIXED order (run-to-run deterministic, like the reference's
+    // serial reduction): split 0 of an output tile stores its
+    // partial, split j > 0 waits on the tile quarter's turnstile for j, reduce-
+    // adds, waits for its writes to complete and passes the turnstile on (the
+    // last split resets it to 0 for the next launch). Splits are claimed in
+    // order (split-outermost unit numbering), so every wait is on a unit claimed
+    // earlier by a resident CTA: no deadlock.
+    const bool reduce = a.flags & kFlagReduce;
+    unsigned int* turn = reduce ? turn_base + 4 * t.tile + q : nullptr;
+    const auto turn_wait = [&] {
+        if (lane == 0 && t.split > 0) {
+            while (ptx::ld_acquire_gpu(turn) != static_cast<uint32_t>(t.split)) __nanosleep(32);
+            ptx::fence_proxy_async_global();
+        }
+    };
+    const auto turn_pass = [&] {
+        if (lane == 0) {
+            ptx::bulk_wait_group<0>();  // this unit's stores / reduce-adds have completed
+            ptx::fence_proxy_async_global();
+            ptx::st_release_gpu(turn, t.split + 1 == a.splits ? 0u : static_cast<uint32_t>(t.split + 1));
+        }
+    };
     if (sdd) {
         for (int z = 0; z < t.nzero; ++z)
             zero_rows<OUT_F32>(a, row_first, t.zero_blk[z] * a.out_col_blk, a.out_col_blk, lane);
     }
     if (t.n_eff == 0) {
-        if (!sdd && !(a.flags & kFlagReduce)) {
-            const int rem = a.cols_out - t.n0;
-            const int w = t.width;
+        const int rem = a.cols_out - t.n0;
+        const int w = t.width;
+        if (!sdd && (!reduce || t.split == 0)) {
             if (rem > 0) zero_rows<OUT_F32>(a, row_first, t.n0, rem < w ? rem : w, lane);
+        }
+        if (reduce) {
+            __threadfence();
+            __syncwarp();
+            turn_wait();
+            turn_pass();
+            __syncwarp();
         }
         return;
     }
@@ -376,6 +409,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
+        if (reduce && c == 0) turn_wait();
         if (lane == 0) {
             int col;
             if (sdd) {
@@ -385,13 +419,17 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
             } else {
                 col = t.n0 + c * kChunkCols;
             }
-            if (a.flags & kFlagReduce)
+            if (reduce && t.split > 0)
                 ptx::tma_reduce_add_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
             else
                 ptx::tma_store_2d(tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
             ptx::bulk_commit_group();
         }
         if constexpr (KCfg<WIDE>::kEpiBufs == 2) bi ^= 1;
+    }
+    if (reduce) {
+        turn_pass();
+        __syncwarp();
     }
 }
 
@@ -436,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(tempty_bar + i, kEpiWarps);
         }
         for (int i = 0; i < kSchedDepth; ++i) {
-            ptx::mbar_init(sfull_bar + i, 1);
-            ptx::mbar_init(sempty_bar + i, 2 + kEpiWarps);  // producer, MMA, epilogue warps
+            ptx::mbar_init(sfull_bar + i, 32);  // every scheduler lane publishes its own list stores
+            ptx::mbar_init(sempty_bar + i, 2 + 32 * kEpiWarps);  // producer, MMA, every epilogue lane
         }
         ptx::mbar_init(claim_bar, 1);
         ptx::fence_barrier_init();
@@ -631,10 +669,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), 0));
             nblk = __shfl_sync(0xffffffffu, nblk, 0);
             unstaged = unstaged || nblk > kListCap;
-            if (lane == 0) SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
-            __syncwarp();
+            // every lane acquires the slot itself (it overwrites list entries the
+            // producer read under the previous phase) and releases its own
+            // stores on sfull below: no reliance on __syncwarp for cross-lane
+            // ordering (compute-sanitizer racecheck reported the list reads as
+            // racing with these stores when only lane 0 waited and arrived)
+            SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
             for (int i = lane; i < nblk && i < kListCap; i += 32) sched_list[sslot * kListCap + i] = __ldcg(src + i);
-            __syncwarp();
             const int prob = __shfl_sync(0xffffffffu, t.prob, 0);
             // the last unit of the launch decoded: nothing reads the mask
             // workspaces any more (every other unit was decoded before its
@@ -651,10 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (lane == 0) {
-                sched_unit[sslot] = t;
-                ptx::mbar_arrive(sfull_bar + sslot);  // release: the list stores above are visible
-            }
+            if (lane == 0) sched_unit[sslot] = t;
+            ptx::mbar_arrive(sfull_bar + sslot);  // release: this lane's list / unit stores are visible
             if (++sslot == kSchedDepth) {
                 sslot = 0;
                 sphase ^= 1;
@@ -789,8 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (true) {
             SD_TWAIT(6, ptx::mbar_wait(sfull_bar + sslot, sphase));
             const Unit t = sched_unit[sslot];
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(sempty_bar + sslot);
+            ptx::mbar_arrive(sempty_bar + sslot);  // each lane releases its own read of the slot
             if (++sslot == kSchedDepth) {
                 sslot = 0;
                 sphase ^= 1;
@@ -798,12 +836,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t.prob < 0) break;
             const GemmArgs& a = L.p[t.prob];
             const CUtensorMap* tmOut = &tms.m[3 * t.prob + 2];
+            unsigned int* turn_base = L.sched + kSchedWords + t.prob * kTurnPerProb;
             if (a.flags & kFlagF32)
                 epilogue_unit<WIDE, true>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr,
-                                          bi, acc_iter, tr);
+                                          bi, acc_iter, turn_base, tr);
             else
                 epilogue_unit<WIDE, false>(a, tmOut, t, q, lane, tmem_base, tfull_bar, tempty_bar, ebuf, ebuf_addr,
-                                           bi, acc_iter, tr);
+                                           bi, acc_iter, turn_base, tr);
             SD_TADD(11, 1);
         }
         if (lane == 0) ptx::bulk_wait_group<0>();
@@ -900,16 +939,14 @@ static bool wide_units(const GemmCall* const* calls, int n) {
 
 void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_wait) {
     if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
-    static bool configured = false;
-    if (!configured) {
+    configure_once_per_device(0, [] {
         check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         KCfg<false>::kSmem),
                    "cudaFuncSetAttribute(max dynamic smem)");
         check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         KCfg<true>::kSmem),
                    "cudaFuncSetAttribute(max dynamic smem, wide)");
-        configured = true;
-    }
+    });
     // dense problems go to the 2-CTA kernel (half the per-SM operand traffic
     // per MAC: tools/gemm2_check.py, +10-25% over this kernel at 4096-8192)
     {
@@ -932,9 +969,9 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     std::memset(&L, 0, sizeof L);
     const int sms = num_sms();
     // split-K for dsd problems with too few output tiles to fill the GPU (e.g.
-    // the MLP's dW, 72 tiles over a 65536-long reduction): fp32 outputs only,
-    // partial sums reduce-added by TMA into the zeroed output (the summation
-    // order across splits is then not fixed; results stay within tolerance).
+    // the MLP's dW, 72 tiles over a 65536-long reduction): fp32 outputs only;
+    // split 0 stores, the others reduce-add in split order behind a per-tile
+    // turnstile, so the result is bit-reproducible run to run.
     // unit width: 128 x 512 (wide) or 128 x 256, one choice per launch
     const bool wide = wide_units(calls, n);
     const int width = wide ? 2 * kBN : kBN;
@@ -953,12 +990,9 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
             red_stages >= 64) {
             int sp = (2 * sms + base - 1) / base;
             sp = std::min(sp, red_stages / 32);
-            if (sp > 1) {
+            if (sp > 1 && base * 4 <= kTurnPerProb) {
                 pa[i].splits = sp;
                 pa[i].flags |= kFlagReduce;
-                check_cuda(cudaMemsetAsync(pa[i].out, 0,
-                                           static_cast<size_t>(pa[i].rows_out) * pa[i].cols_out * sizeof(float), s),
-                           "cudaMemsetAsync(split-K output)");
             }
         }
         cost[i] = static_cast<float>(red_stages) / pa[i].splits;  // stages per unit (upper bound)
@@ -1010,7 +1044,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
 #endif
     const int grid = total < cap ? total : cap;
     if (grid <= 0) return;
-    L.sched = sched_slot();
+    L.sched = sched_slot(s);
     L.trace_id = static_cast<int>(sd_launch_count());
     L.no_wait = no_wait && !(g_tuning & kTuneNoEarlyBackward);
     // bound mask workspaces read by this launch (lists, counts, row orders)

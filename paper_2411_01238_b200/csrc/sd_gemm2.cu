@@ -46,7 +46,8 @@ constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
 constexpr int kNumBars = 2 * kStages2 + 4;
 constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
 constexpr int kSmemBytes2 = kOffTmemSlot + 16 + 1024;
-static_assert(kSmemBytes2 <= 232448, "shared memory budget");
+constexpr int kMaxOwnUnits = 512;  // static smem: keep bits of a CTA's units (kFlagOutMask)
+static_assert(kSmemBytes2 + kMaxOwnUnits <= 232448, "shared memory budget (dynamic + static own_bits)");
 
 __device__ __forceinline__ void tma_load_2sm_3d(const void* tmap, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
                                                 int32_t c2) {
@@ -89,6 +90,7 @@ struct Pair2Args {
     int pair_stride;
     int no_wait;  // skip griddepcontrol.wait (see launch_gemms)
     unsigned int* release;  // mask workspace read (kFlagOutMask words): +1 per CTA at exit
+    int own_cap;            // units whose keep bits are read up front (<= kMaxOwnUnits; 0: per chunk)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
+    __syncthreads();  // also a CTA barrier: compute-sanitizer racecheck does not treat barrier.cluster as one
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (!P.no_wait) ptx::pdl_wait();
@@ -157,10 +160,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     // 128-column blocks) for every unit it will run, read once up front, so the
     // mask workspace is released now instead of at exit and the next mask
     // generation overlaps this grid (more than kMaxOwnUnits units: at exit)
-    constexpr int kMaxOwnUnits = 512;
     __shared__ uint8_t own_bits[kMaxOwnUnits];
     const int own_units = (num_units - cluster_id + n_clusters - 1) / n_clusters;
-    const bool bits_up_front = (a.flags & kFlagOutMask) && own_units <= kMaxOwnUnits;
+    const bool bits_up_front = (a.flags & kFlagOutMask) && own_units <= P.own_cap;
     if (bits_up_front) {
         for (int k = threadIdx.x; k < own_units; k += kThreads) {
             int prow, ct;
@@ -387,12 +389,10 @@ bool gemm2_supported(const GemmArgs& a) {
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
                   bool no_wait, unsigned int* release) {
-    static bool configured = false;
-    if (!configured) {
+    configure_once_per_device(1, [] {
         check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2),
                    "cudaFuncSetAttribute(gemm2 smem)");
-        configured = true;
-    }
+    });
     Pair2Args P;
     std::memset(&P, 0, sizeof P);
     P.g = g;
@@ -403,6 +403,7 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     P.pair_stride = pair_stride;
     P.no_wait = no_wait && !(tuning() & kTuneNoEarlyBackward) ? 1 : 0;
     P.release = release;
+    P.own_cap = (tuning() & kTuneNoOwnBits) ? 0 : kMaxOwnUnits;
     const int units = P.n_pair_rows * P.n_col_tiles;
     int clusters = std::min(units, num_sms() / 2);
     if (clusters <= 0) return;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/sparsedrop_b200.h"
@@ -21,6 +22,10 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 int num_sms();
+// Runs `fn` once per (key, current device) under a lock: kernel attributes such
+// as the dynamic shared-memory limit are per device context. Keys: 0 sd_gemm,
+// 1 sd_gemm2, 2 mask kernels, 3 elementwise kernels.
+void configure_once_per_device(int key, const std::function<void()>& fn);
 void note_launch(uint64_t n = 1);
 
 // ---------------------------------------------------------------- mask readers
@@ -59,7 +64,7 @@ enum GemmFlags : uint32_t {
     kFlagBMN = 2u,  // B is MN-major (contiguous along the output columns), else K-major
     kFlagSDD = 4u,  // output-block skipping (sdd) instead of reduction-block skipping (dsd)
     kFlagF32 = 8u,  // fp32 output, else bf16
-    kFlagReduce = 16u,  // split-K: the epilogue reduce-adds into a pre-zeroed fp32 output
+    kFlagReduce = 16u,  // split-K: split 0 stores, split j > 0 reduce-adds after split j - 1 (fixed order)
     kFlagOutMask = 32u,  // 2-CTA dense only: output blocks dropped in `words` (128x128, mask_cols
                          // per row) are written as +0.0 (dX at low p: masked dense, see sd_capi.cu)
 };
@@ -98,9 +103,17 @@ inline int gemm_units(const GemmArgs& a) {
 }
 
 // Zeroed {next unit, CTAs done, units decoded, spare} counters for one
-// persistent-kernel launch (ring of slots per device, re-armed by the last CTA
-// of the launch that used it).
-unsigned int* sched_slot();
+// persistent-kernel launch, followed by kTurnstiles split-K turnstiles (two
+// problems x up to kTurnPerProb/4 output tiles x 4 epilogue row quarters). A
+// ring of slots per device, re-armed by the last CTA of the launch that used
+// it (turnstiles are reset by each tile's last split). A launch captured into a
+// CUDA graph gets a dedicated slot that is never handed out again (it is
+// replayed later, possibly beside eager launches).
+constexpr int kSchedWords = 64;
+constexpr int kTurnPerProb = 2048;
+constexpr int kTurnstiles = 2 * kTurnPerProb;
+constexpr int kSlotWords = kSchedWords + kTurnstiles;
+unsigned int* sched_slot(cudaStream_t s);
 
 // A fully validated, ready-to-launch GEMM problem (tensor maps encoded).
 struct GemmCall {
@@ -122,6 +135,8 @@ enum TuneFlags : int {
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
     kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
     kTuneNoMaskedDense = 1024,   // low-p dX stays on the sdd kernel instead of the masked 2-CTA dense GEMM
+    kTuneNoOwnBits = 2048,       // masked 2-CTA dX reads keep bits per chunk and releases at exit (the
+                                 // > kMaxOwnUnits fallback, forced for tests)
 };
 int tuning();
 void set_tuning(int t);

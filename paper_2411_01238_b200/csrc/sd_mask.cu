@@ -115,6 +115,10 @@ __device__ __forceinline__ void finish_block(const PlanArgs& a) {
             *a.rel = 0u;
             *a.m.ticket = 0u;
             __threadfence();
+            // counter mode never waited for the preceding grid: the last block
+            // out does, so this grid's completion implies its predecessor's
+            // under the documented PDL semantics (not only by transitivity)
+            if (a.rel_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
         }
     }
 }
@@ -460,6 +464,8 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     if (threadIdx.x == 0) {
         if (a.rel) *a.rel = 0u;  // every block has passed its wait: next round of readers
         *a.m.ticket = 0u;        // re-arm for the next launch on this workspace
+        // counter mode: complete only after the preceding grid (see finish_block)
+        if (a.rel_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
@@ -536,12 +542,10 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     const int inline_ints = a.inline_order ? 2 * (m.block_rows + m.block_cols) + bins : 0;
     const size_t smem = static_cast<size_t>(std::max({bins, chunks, inline_ints})) * sizeof(int);
     if (smem > 48 * 1024) {
-        static bool raised = false;
-        if (!raised) {
+        configure_once_per_device(2, [] {
             check_cuda(cudaFuncSetAttribute(mask_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                        "mask_plan_kernel smem");
-            raised = true;
-        }
+        });
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -67,7 +67,7 @@ class SparseDropMLP:
         self.dact = torch.empty(m, hdim, dtype=torch.bfloat16, device=dev)  # dL/dh, fc1's output grad
         # fc1: x -> h (plan writes y = h); fc2: act -> y
         self.fc1 = LayerPlan(x, w1, self.dact, p)
-        self.fc2 = LayerPlan(self.act, w2, dy, p)
+        self.fc2 = LayerPlan(self.act, w2, dy, p, dy_ready=True)  # dy is the caller's, ready before the step
 
     def step(self, step_seed: int, stream=None):
         f1, f2 = self.fc1, self.fc2

@@ -34,7 +34,8 @@ class HostLayerPipeline:
             xd = torch.empty_like(x_host, device=dev)
             wd = torch.empty_like(w_host, device=dev)
             dyd = torch.empty_like(dy_host, device=dev)
-            plan = LayerPlan(xd, wd, dyd, p, row_block_offset=row_block_offset, dw_dtype=dw_dtype)
+            plan = LayerPlan(xd, wd, dyd, p, row_block_offset=row_block_offset, dw_dtype=dw_dtype,
+                             dy_ready=True)  # dY is uploaded (h2d stream) before the forward
             self.slots.append({
                 "in": (xd, wd, dyd), "plan": plan,
                 "h2d": torch.cuda.Event(), "cmp": torch.cuda.Event(), "d2h": torch.cuda.Event(),

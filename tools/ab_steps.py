@@ -27,7 +27,7 @@ for i in range(3):
     x = torch.randn(S, S, device="cuda").to(torch.bfloat16)
     w = torch.randn(S, S, device="cuda").to(torch.bfloat16)
     dy = torch.randn(S, S, device="cuda").to(torch.bfloat16)
-    plans.append(sd.LayerPlan(x, w, dy, P))
+    plans.append(sd.LayerPlan(x, w, dy, P, dy_ready=True))
 
 
 DENSE = os.environ.get("DENSE") == "1"  # time the dense step (dense_forward + dense_backward) instead

@@ -94,7 +94,7 @@ def layer_cfg(name, M, N, K, ps, steps, slab_rows=512):
     dense_ms = None
     flops = 3 * 2 * M * N * K
     for p in ps:
-        plan = sd.LayerPlan(x, w, dy, p)
+        plan = sd.LayerPlan(x, w, dy, p, dy_ready=True)
         ms = timed(lambda i: (plan.forward(sd.effective_seed(0, i, 0)), plan.backward()), steps)
         keep = plan.mask.keep_count() / plan.mask.total_blocks()
         if dense_ms is None:

@@ -61,7 +61,7 @@ def main():
         for p in [float(v) for v in args.sparsity.split(",")]:
             for method in ("dense", "dropout_dense", "block_dropout_dense", "sparsedrop"):
                 if method == "sparsedrop":
-                    lay = sd.LayerPlan(x, w, dy, p)
+                    lay = sd.LayerPlan(x, w, dy, p, dy_ready=True)
                     fwd = lambda i, lay=lay: lay.forward(sd.effective_seed(0, i, 0))  # noqa: E731
                     bwd = lambda i, lay=lay: lay.backward()  # noqa: E731
                 else:

@@ -19,7 +19,7 @@ dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
 y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 dx = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
 dw = torch.empty(K, N, device="cuda", dtype=torch.float32)
-plan = sd.LayerPlan(x, w, dy, P)
+plan = sd.LayerPlan(x, w, dy, P, dy_ready=True)
 plan.forward(0)
 m = plan.mask
 s = sd.dropout_scale(P)

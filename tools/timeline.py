@@ -24,7 +24,7 @@ BACK_TO_BACK = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # steps per timed b
 x = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 w = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 dy = torch.randn(S, S, device="cuda").to(torch.bfloat16)
-plan = sd.LayerPlan(x, w, dy, P)
+plan = sd.LayerPlan(x, w, dy, P, dy_ready=True)
 flush = torch.empty(512 * 1024 * 1024 // 4, device="cuda")
 g = np.zeros(256 * 4, dtype=np.uint64)
 mk = np.zeros(256 * 4, dtype=np.uint64)

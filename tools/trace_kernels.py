@@ -25,7 +25,7 @@ M, N, K = (int(v) for v in S.split(",")) if "," in S else (int(S),) * 3
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 w = torch.randn(K, N, device="cuda").to(torch.bfloat16)
 dy = torch.randn(M, N, device="cuda").to(torch.bfloat16)
-plan = sd.LayerPlan(x, w, dy, P)
+plan = sd.LayerPlan(x, w, dy, P, dy_ready=True)
 plan.forward(0)
 torch.cuda.synchronize()
 m = plan.mask
