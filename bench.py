@@ -58,6 +58,11 @@ def parse_args():
                     help="N>1: dW computed in this many row slabs, each all-reduced while the next slab and dX run")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (CI check of the data-parallel path)")
+    ap.add_argument("--config", choices=["cfg2", "cfg5"], default=None,
+                    help="cfg2 = configs[1] (4096^3 per GPU, the N=1 default); cfg5 = configs[4] (M=524288, "
+                         "K=N=8192 row-sharded over the ranks, strong scaling; the N>1 default)")
+    ap.add_argument("--m-global", type=int, default=524288, help="cfg5: global M (reduced only for CI tests)")
+    ap.add_argument("--kn", type=int, default=8192, help="cfg5: K = N (reduced only for CI tests)")
     return ap.parse_args()
 
 
@@ -232,10 +237,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "cfg2" if world == 1 else "cfg5"
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    if world > 1:
+        # NCCL communicator lines (rank count, transport) on stderr, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     import torch
     import torch.distributed as dist
@@ -251,6 +262,11 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
+    if args.config == "cfg5":
+        run_cfg5(args, rank, world, dev_index, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     def barrier():
         if world > 1:
@@ -634,6 +650,208 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ configs[4]: row-sharded data parallel
+
+def cfg5_config(m_global, kn, p, world, nparts, backend):
+    return {
+        "workload": f"configs[4]: row-sharded data-parallel SparseDrop linear fwd+bwd, M={m_global} (global, "
+                    f"M/{world} rows per GPU), K=N={kn}, 128x128 blocks, p={p}, one dW all-reduce per step",
+        "M_global": m_global, "M_per_gpu": m_global // world, "N": kn, "K": kn, "m_blk": 128, "k_blk": 128,
+        "p": p, "seed": 0,
+        "dtypes": {"x/w/dy/y/dx": "bf16", "dw": "fp32 (all-reduced)", "accumulate": "fp32"},
+        "l2": "inputs larger than L2 (each rank's X and dY exceed the 126 MB L2 at every N <= 8)",
+        "parallelism": (f"dp{world}: rank g owns global rows [g*M/{world}, (g+1)*M/{world}), shard-local masks "
+                        f"(bit-identical to the global mask rows), W replicated; dW in {nparts} row slabs, each "
+                        + ("sum-all-reduced through the library's NCCL communicator (C-ABI "
+                           "sd_layer_plan_backward_allreduce) on a comm stream while the next slab and dX compute"
+                           if backend == "nccl" else
+                           "all-reduced with torch.distributed (gloo; CI path, several ranks on one GPU)"))
+        if world > 1 else "single GPU (the strong-scaling baseline: the whole M on one B200)",
+    }
+
+
+def run_cfg5(args, rank, world, dev_index, dev):
+    """configs[4]: M=524288, K=N=8192 strong-scaled over the ranks.
+    value = 3*2*M*N*K (dense-equivalent, whole job) / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_01238_b200 as sd
+    from paper_2411_01238_b200.sharding import shard_rows
+
+    KN, MG, p = args.kn, args.m_global, args.p
+    shard = shard_rows(MG, 128, world, rank)
+    M = shard.rows
+    nparts = max(1, args.dw_parts)
+    use_lib_comm = world > 1 and args.dist_backend == "nccl"
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def synth(r, c, g):
+        out = torch.empty(r, c, dtype=torch.bfloat16, device=dev)
+        step = max(1, (1 << 28) // c)  # chunks of <= 256 M elements (bounded fp32 temporaries)
+        for r0 in range(0, r, step):
+            r1 = min(r, r0 + step)
+            u = torch.rand(r1 - r0, c, generator=g, device=dev)
+            sign = torch.where(torch.rand(r1 - r0, c, generator=g, device=dev) < 0.5, -1.0, 1.0)
+            out[r0:r1] = ((0.25 + u) * sign).to(torch.bfloat16)
+            del u, sign
+        return out
+
+    gen_w = torch.Generator(device=dev)
+    gen_w.manual_seed(99)  # W replicated: the same on every rank
+    x, w, dy = synth(M, KN, gen), synth(KN, KN, gen_w), synth(M, KN, gen)
+    plan = sd.LayerPlan(x, w, dy, p, row_block_offset=shard.row_block_offset, dy_ready=True)
+    comm = None
+    if use_lib_comm:
+        obj = [sd.Communicator.new_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = sd.Communicator(world, rank, obj[0])
+    comm_stream = torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream()
+
+    def step(i):
+        plan.forward(seed=sd.effective_seed(0, i, 0))
+        if world == 1:
+            plan.backward()
+        elif comm is not None:
+            plan.backward_allreduce(comm, nparts, stream=cur, comm_stream=comm_stream)
+        else:
+            for part in range(nparts):
+                slab = plan.backward_dw_part(part, nparts)
+                comm_stream.wait_stream(cur)
+                with torch.cuda.stream(comm_stream):
+                    dist.all_reduce(slab)
+            plan.backward_dx()
+            cur.wait_stream(comm_stream)
+
+    def compute_only(i):
+        plan.forward(seed=sd.effective_seed(0, i, 0))
+        if world == 1:
+            plan.backward()
+        else:
+            for part in range(nparts):
+                plan.backward_dw_part(part, nparts)
+            plan.backward_dx()
+
+    def allreduce_only(i):
+        if comm is not None:
+            comm.allreduce_sum(plan.dw, stream=cur)
+        elif world > 1:
+            dist.all_reduce(plan.dw)
+
+    def timed(fn, steps, warmup, preroll_s):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn(0)
+        torch.cuda.synchronize()
+        est = max(time.perf_counter() - t0, 1e-5)
+        n_pre = int(max_over_ranks(float(min(max(preroll_s / est, 0), 200))))
+        for j in range(n_pre + warmup):
+            fn(j)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        l0 = sd.launch_count()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for i in range(steps):
+            fn(warmup + i)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        barrier()
+        return max_over_ranks(ms), sd.launch_count() - l0
+
+    with ClockSampler(dev_index) as clk:
+        ms, launches = timed(step, args.steps, args.warmup, args.preroll if args.preroll > 0 else 0.0)
+    ms_compute, _ = timed(compute_only, max(3, args.steps // 2), 2, 0.0)
+    ms_ar = timed(allreduce_only, max(3, args.steps // 2), 2, 0.0)[0] if world > 1 else 0.0
+    keep_local = plan.mask.keep_count()
+    keep_t = torch.tensor([float(keep_local)], dtype=torch.float64,
+                          device=dev if args.dist_backend == "nccl" else "cpu")
+    if world > 1:
+        dist.all_reduce(keep_t)
+    keep = float(keep_t.item()) / ((MG // 128) * (KN // 128))
+    flops = 3 * 2 * MG * KN * KN
+    value = flops / (ms * 1e-3) / 1e12
+    exposed = max(0.0, ms - ms_compute)
+    comm_info = {
+        "allreduce_ms": ms_ar, "allreduce_bytes": KN * KN * 4, "compute_only_ms_per_step": ms_compute,
+        "exposed_comm_ms": exposed,
+        "overlap_fraction": (min(1.0, max(0.0, 1.0 - exposed / ms_ar)) if ms_ar > 0 else None),
+        "busbw_gbps": (KN * KN * 4 * 2 * (world - 1) / world / (ms_ar * 1e-3) / 1e9) if ms_ar > 0 else None,
+        "path": ("C-ABI sd_layer_plan_backward_allreduce (library-owned NCCL communicator, NCCL "
+                 f"{sd.Communicator.nccl_version()})" if comm is not None else
+                 ("torch.distributed gloo (CI)" if world > 1 else "none (single GPU)")),
+        "note": "device-timed, max over ranks: allreduce_ms = the dW all-reduce alone; compute_only = the "
+                "same step without it; overlap_fraction = 1 - (step - compute_only) / allreduce",
+    }
+    # e2e through the public API with host buffers (pinned), every step
+    e2e = None
+    if not args.no_e2e:
+        from paper_2411_01238_b200.pipeline import HostLayerPipeline
+
+        xh, wh, dyh = x.cpu().pin_memory(), w.cpu().pin_memory(), dy.cpu().pin_memory()
+        del plan
+        torch.cuda.empty_cache()
+        pipe = HostLayerPipeline(xh, wh, dyh, p, row_block_offset=shard.row_block_offset, device=dev)
+        ar = None
+        if world > 1:
+            ar = ((lambda t: comm.allreduce_sum(t)) if comm is not None else (lambda t: dist.all_reduce(t)))
+        n_e2e = 3
+        for i in range(2):
+            pipe.step(i, ar)
+        pipe.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(pipe.s_h2d)
+        pipe.s_cmp.wait_stream(pipe.s_h2d)
+        for i in range(n_e2e):
+            pipe.step(2 + i, ar)
+        pipe.s_d2h.wait_stream(pipe.s_cmp)
+        pipe.s_d2h.wait_stream(pipe.s_h2d)
+        ev1.record(pipe.s_d2h)
+        pipe.synchronize()
+        ms_e2e = max_over_ranks(ev0.elapsed_time(ev1)) / n_e2e
+        e2e = {"value": flops / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
+               "path": "HostLayerPipeline -> LayerPlan (C-ABI), pinned host X/W/dY in and Y/dX/dW out every "
+                       "step on every rank (per-rank bytes above)" + (", dW all-reduced" if world > 1 else "")}
+        del pipe
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random_matrix distribution, on device)",
+            "config": cfg5_config(MG, KN, p, world, nparts, args.dist_backend),
+            "keep_fraction": keep, "executed_tflops": value * keep,
+            "comm": comm_info, "gpu_launches": launches,
+            "gpu_launches_note": "per step: mask, forward, " + (f"{nparts} dW slabs, dX" if world > 1 else
+                                                               "fused dW+dX (or dW + masked dX at low p)"),
+            "cpu_baseline": None,
+            "cpu_baseline_note": "the reference CPU path is timed in the configs[1] line (N=1 default run)",
+            "e2e": e2e, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
 
 
 if __name__ == "__main__":

@@ -205,6 +205,33 @@ SD_API int sd_layer_plan_dense_backward(sd_layer_plan* plan, void* stream);
 SD_API int sd_layer_plan_set_options(sd_layer_plan* plan, int32_t options);
 SD_API int sd_layer_plan_destroy(sd_layer_plan* plan);
 
+/* ---- Data-parallel backward over row shards (the reference's
+ * decomposition: tile rows are independent, gemm.hpp:84-100, and the keep
+ * decision depends only on (seed, global row, column), block_mask.cpp:70).
+ * Rank g owns rows [g*M/G, (g+1)*M/G) of X, dY, Y, dX (its plan is created with
+ * row_block_offset = first global block row); W is replicated; each rank's dW
+ * is the partial sum over its rows and ONE sum all-reduce (NCCL, NVLink)
+ * gives every rank the full dW. The library owns the NCCL communicator; NCCL
+ * is loaded at run time (the copy already in the process if any, else
+ * libnccl.so.2; SD_NCCL_LIBRARY overrides). */
+typedef struct sd_comm sd_comm;
+#define SD_COMM_ID_BYTES 128
+/* rank 0: a fresh 128-byte NCCL unique id, to be broadcast by the caller */
+SD_API int sd_comm_unique_id(void* id_out);
+/* every rank, on its own device (cudaSetDevice first): collective */
+SD_API int sd_comm_init(sd_comm** comm, int32_t nranks, int32_t rank, const void* id);
+SD_API int sd_comm_destroy(sd_comm* comm);
+SD_API int sd_comm_nccl_version(int32_t* version);
+/* in-place sum all-reduce of `count` elements (SD_DTYPE_F32 / SD_DTYPE_BF16) */
+SD_API int sd_comm_allreduce_sum(sd_comm* comm, void* buf, size_t count, int32_t dtype, void* stream);
+/* backward(layer, ctx, dy) of a row shard (layer.hpp:128-162) with the dW
+ * all-reduce: dW in `nparts` row slabs (mask-column blocks, bit-identical to
+ * the full dW's rows), slab i all-reduced on `comm_stream` while slab i+1 and
+ * then dX compute on `stream`; `stream` waits for the last all-reduce before
+ * anything enqueued after this call (comm_stream NULL: all on `stream`). */
+SD_API int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t nparts, void* stream,
+                                            void* comm_stream);
+
 /* The MLP block's activation between two SparseDrop Linears (configs[2]):
  * exact GELU and its backward, one HBM pass each over n bf16 values
  * (n % 8 == 0, 16-byte aligned). act = h*Phi(h); dh = grad*(Phi(h) + h*phi(h)). */

@@ -7,6 +7,7 @@ include/sparsedrop_b200.h); this package is the host-side mirror.
 """
 from .api import (  # noqa: F401
     BlockMask,
+    Communicator,
     DropoutSpec,
     KernelCounters,
     LayerContext,

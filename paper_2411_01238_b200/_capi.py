@@ -83,6 +83,12 @@ PROTOTYPES = {
     "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_set_options": (ctypes.c_int, [_P, _I]),
     "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
+    "sd_comm_unique_id": (ctypes.c_int, [_P]),
+    "sd_comm_init": (ctypes.c_int, [ctypes.POINTER(_P), _I, _I, _P]),
+    "sd_comm_destroy": (ctypes.c_int, [_P]),
+    "sd_comm_nccl_version": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
+    "sd_comm_allreduce_sum": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _I, _P]),
+    "sd_layer_plan_backward_allreduce": (ctypes.c_int, [_P, _P, _I, _P, _P]),
     "sd_gelu_forward": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "sd_gelu_backward": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P]),
     "sd_gemm_ex": (ctypes.c_int, [_P, _I, _P, _I, _P, _I, _I, _I, _I, ctypes.c_float, _P]),

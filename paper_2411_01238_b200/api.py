@@ -499,6 +499,16 @@ class LayerPlan:
         C, kb = self.mask.block_cols(), self.mask.k_blk()
         return self.dw[(C * part // nparts) * kb:(C * (part + 1) // nparts) * kb]
 
+    def backward_allreduce(self, comm: "Communicator", nparts: int = 2, stream=None, comm_stream=None):
+        """Row-shard backward with the dW all-reduce behind the C-ABI
+        (sd_layer_plan_backward_allreduce): dW in `nparts` row slabs, each
+        summed over the ranks by NCCL on `comm_stream` while the next slab and
+        dX compute on `stream`; `stream` then waits for the last all-reduce."""
+        cs = ctypes.c_void_p(_stream(comm_stream)) if comm_stream is not None else None
+        check(_lib().sd_layer_plan_backward_allreduce(self._plan, comm._c, nparts, ctypes.c_void_p(_stream(stream)),
+                                                      cs))
+        return self.dx, self.dw
+
     def backward_dx(self, stream=None):
         check(_lib().sd_layer_plan_backward_dx(self._plan, ctypes.c_void_p(_stream(stream))))
         return self.dx
@@ -516,6 +526,53 @@ class LayerPlan:
             if self._plan:
                 _lib().sd_layer_plan_destroy(self._plan)
                 self._plan = ctypes.c_void_p()
+        except Exception:
+            pass
+
+
+class Communicator:
+    """The library's NCCL communicator (sd_comm_*) for the data-parallel
+    backward. `unique_id` (128 bytes) comes from rank 0's
+    Communicator.new_unique_id() and is broadcast by the caller (e.g. with
+    torch.distributed.broadcast_object_list)."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def new_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(Communicator.ID_BYTES)
+        check(_lib().sd_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes):
+        if len(unique_id) != self.ID_BYTES:
+            raise ValueError(f"unique_id must be {self.ID_BYTES} bytes")
+        self._c = ctypes.c_void_p()
+        self.nranks, self.rank = nranks, rank
+        check(_lib().sd_comm_init(ctypes.byref(self._c), nranks, rank, ctypes.create_string_buffer(unique_id,
+                                                                                                    self.ID_BYTES)))
+
+    def allreduce_sum(self, t: torch.Tensor, stream=None) -> torch.Tensor:
+        if t.dtype not in (torch.float32, torch.bfloat16) or not t.is_contiguous():
+            raise ValueError("allreduce_sum: contiguous fp32 or bf16 tensor")
+        check(_lib().sd_comm_allreduce_sum(self._c, t.data_ptr(), t.numel(), _dtype_code(t.dtype),
+                                           ctypes.c_void_p(_stream(stream))))
+        return t
+
+    @staticmethod
+    def nccl_version() -> int:
+        v = ctypes.c_int32(0)
+        check(_lib().sd_comm_nccl_version(ctypes.byref(v)))
+        return int(v.value)
+
+    def close(self):
+        if self._c:
+            check(_lib().sd_comm_destroy(self._c))
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
         except Exception:
             pass
 

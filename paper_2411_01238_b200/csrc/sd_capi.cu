@@ -159,6 +159,7 @@ CUtensorMap mnmajor_map(const void* p, int mn, int red) { return make_tmap_mn_at
 }  // namespace
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 void check_cuda(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(SD_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
@@ -648,6 +649,7 @@ GemmCall prep_layer_dw_part(const GemmCall& full, const void* x, const sd_block_
     g.args.list_cnt = full.args.list_cnt + kb0;
     g.args.list_idx = full.args.list_idx + static_cast<int64_t>(kb0) * full.args.list_stride;
     g.args.row_order = nullptr;
+    g.args.split_rows = full.args.rows_out;  // the full dW's split-K factor (same summation order)
     return g;
 }
 
@@ -721,6 +723,14 @@ struct sd_layer_plan {
     // order as in the sdd kernel: bit-identical)
     sd::GemmCall dx_masked;
     bool dx_masked_ok = false;
+    // data-parallel backward (sd_layer_plan_backward_allreduce): one event per
+    // dW slab (compute -> comm stream) and one for the last all-reduce
+    std::vector<cudaEvent_t> slab_done;
+    cudaEvent_t reduced = nullptr;
+    ~sd_layer_plan() {
+        for (cudaEvent_t e : slab_done) cudaEventDestroy(e);
+        if (reduced) cudaEventDestroy(reduced);
+    }
 };
 
 namespace {
@@ -746,6 +756,19 @@ bool use_masked_dx(const sd_layer_plan* plan) {
 // wave leaves idle. Without the declaration every backward waits for the
 // preceding grid (a caller kernel writing dY may trigger early under PDL).
 // Consumed by the first backward launch.
+// dW split into `nparts` row slabs by mask-column blocks (cached per nparts).
+void prepare_dw_parts(sd_layer_plan* plan, int nparts) {
+    if (plan->dw_parts == nparts) return;
+    const int cblocks = plan->mask.block_cols;
+    plan->dw_part.clear();
+    for (int i = 0; i < nparts; ++i) {
+        const int kb0 = static_cast<int>(static_cast<int64_t>(cblocks) * i / nparts);
+        const int kb1 = static_cast<int>(static_cast<int64_t>(cblocks) * (i + 1) / nparts);
+        plan->dw_part.push_back(prep_layer_dw_part(plan->dw, plan->x, &plan->mask, plan->m, plan->k, plan->n, kb0, kb1));
+    }
+    plan->dw_parts = nparts;
+}
+
 bool take_no_wait(sd_layer_plan* plan, cudaStream_t s) {
     const bool ok = plan->dy_ready && plan->early_backward && plan->fwd_mark == sd_launch_count() &&
                     plan->fwd_stream == s;
@@ -982,17 +1005,51 @@ int sd_layer_plan_backward_dw_part(sd_layer_plan* plan, int32_t part, int32_t np
         if (nparts < 1 || part < 0 || part >= nparts || nparts > cblocks)
             fail(SD_ERANGE, "backward_dw_part: part " + str(part) + " of " + str(nparts) + " out of range for " +
                                 str(cblocks) + " mask columns");
-        if (plan->dw_parts != nparts) {
-            plan->dw_part.clear();
-            for (int i = 0; i < nparts; ++i) {
-                const int kb0 = static_cast<int>(static_cast<int64_t>(cblocks) * i / nparts);
-                const int kb1 = static_cast<int>(static_cast<int64_t>(cblocks) * (i + 1) / nparts);
-                plan->dw_part.push_back(prep_layer_dw_part(plan->dw, plan->x, &plan->mask, plan->m, plan->k,
-                                                           plan->n, kb0, kb1));
-            }
-            plan->dw_parts = nparts;
-        }
+        prepare_dw_parts(plan, nparts);
         launch_gemm(plan->dw_part[part], as_stream(stream), take_no_wait(plan, as_stream(stream)));
+    });
+}
+
+int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t nparts, void* stream,
+                                     void* comm_stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        if (!comm) fail(SD_EINVAL, "sd_layer_plan_backward_allreduce: null communicator");
+        const int cblocks = plan->mask.block_cols;
+        if (nparts < 1 || nparts > cblocks)
+            fail(SD_ERANGE, "backward_allreduce: nparts " + str(nparts) + " out of range for " + str(cblocks) +
+                                " mask columns");
+        prepare_dw_parts(plan, nparts);
+        const cudaStream_t s = as_stream(stream);
+        const cudaStream_t cs = comm_stream ? as_stream(comm_stream) : s;
+        while (static_cast<int>(plan->slab_done.size()) < nparts) {
+            cudaEvent_t e;
+            check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            plan->slab_done.push_back(e);
+        }
+        if (!plan->reduced) check_cuda(cudaEventCreateWithFlags(&plan->reduced, cudaEventDisableTiming), "cudaEventCreate");
+        const bool f32 = plan->dw.args.flags & kFlagF32;
+        const size_t el = f32 ? 4 : 2;
+        const bool nw = take_no_wait(plan, s);
+        // dW slab by slab (mask-column blocks, the same tiles and reduction
+        // order as the full dW): slab i's all-reduce runs on the comm stream
+        // while slab i+1 and then dX compute on `stream`
+        for (int i = 0; i < nparts; ++i) {
+            const GemmCall& g = plan->dw_part[i];
+            launch_gemm(g, s, i == 0 && nw);
+            if (cs != s) {
+                check_cuda(cudaEventRecord(plan->slab_done[i], s), "cudaEventRecord(dW slab)");
+                check_cuda(cudaStreamWaitEvent(cs, plan->slab_done[i], 0), "cudaStreamWaitEvent(dW slab)");
+            }
+            comm_allreduce_sum(comm, g.args.out, static_cast<size_t>(g.args.rows_out) * g.args.cols_out,
+                               f32 ? SD_DTYPE_F32 : SD_DTYPE_BF16, cs);
+            (void)el;
+        }
+        launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, s);
+        if (cs != s) {
+            check_cuda(cudaEventRecord(plan->reduced, cs), "cudaEventRecord(all-reduce)");
+            check_cuda(cudaStreamWaitEvent(s, plan->reduced, 0), "cudaStreamWaitEvent(all-reduce)");
+        }
     });
 }
 

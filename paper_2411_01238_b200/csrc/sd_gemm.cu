@@ -985,12 +985,19 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         const int base = pa[i].n_row_tiles * pa[i].n_col_units;
         const bool sdd = pa[i].flags & kFlagSDD;
         const int red_stages = pa[i].red / kBK;
-        const int split_below = wide ? sms : 2 * sms;  // a wide unit carries two narrow units' work
-        if (!(g_tuning & kTuneNoSplitK) && !sdd && (pa[i].flags & kFlagF32) && base < split_below &&
+        // The split count is a function of the PROBLEM only (its 128 x 256
+        // tile count, or that of the full problem a row slab belongs to), never
+        // of the launch's unit width or of slabbing: the splits fix the fp32
+        // summation order, so the wide and narrow kernels and the dW row slabs
+        // of the data-parallel backward stay bit-identical to the full dW.
+        const int split_rows = pa[i].split_rows > 0 ? pa[i].split_rows : pa[i].rows_out;
+        const int base_narrow = (split_rows / kBM) * ((pa[i].cols_out + kBN - 1) / kBN);
+        if (!(g_tuning & kTuneNoSplitK) && !sdd && (pa[i].flags & kFlagF32) && base_narrow < 2 * sms &&
             red_stages >= 64) {
-            int sp = (2 * sms + base - 1) / base;
+            int sp = (2 * sms + base_narrow - 1) / base_narrow;
             sp = std::min(sp, red_stages / 32);
-            if (sp > 1 && base * 4 <= kTurnPerProb) {
+            if (sp > 1) {
+                if (base * 4 > kTurnPerProb) fail(SD_ERUNTIME, "split-K turnstile capacity exceeded");
                 pa[i].splits = sp;
                 pa[i].flags |= kFlagReduce;
             }

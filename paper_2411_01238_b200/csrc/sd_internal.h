@@ -20,6 +20,7 @@ struct Error {
 };
 
 [[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const std::string& msg);  // sd_last_error() of the calling thread
 void check_cuda(cudaError_t e, const char* what);
 int num_sms();
 // Runs `fn` once per (key, current device) under a lock: kernel attributes such
@@ -93,6 +94,8 @@ struct GemmArgs {
     int splits;        // dsd split-K factor (>= 1): each unit reduces a contiguous 1/splits of its list
     int tail_rows;     // the last tail_rows tile rows (lightest, end of the queue) use half-width units
     float keep_hint;   // nominal kept fraction of the mask (1 - p) when known, else < 0
+    int split_rows;    // rows of the full problem that fix the split-K factor (0: rows_out; a dW row
+                       // slab passes the full dW's rows so its reduction order equals the full call's)
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
@@ -170,5 +173,10 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
 // bf16 [red][mn] operand (mn contiguous, row pitch ld) as 3D (64, red, mn / 64): box = 128 mn
 // x 64 red in two atom-major 8 KB SW128 atoms; coordinates (0, red0, mn0 / 64).
 CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld);
+
+// ---------------------------------------------------------------- NCCL (sd_comm.cu)
+// In-place sum all-reduce of `count` elements (SD_DTYPE_*) on stream s.
+void comm_allreduce_sum(sd_comm* c, void* buf, size_t count, int dtype, cudaStream_t s);
+int comm_nranks(const sd_comm* c);
 
 }  // namespace sd

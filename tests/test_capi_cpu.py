@@ -123,3 +123,21 @@ def test_flops(lib):
     # gemm.hpp:222-228
     assert lib.sd_flops_effective(1024, 1024, 128, 128, 128, 25, 0) == 2 * 1024 * 128 * 128 * 25
     assert lib.sd_flops_effective(1024, 512, 128, 128, 128, 25, 1) == 2 * 512 * 128 * 128 * 25
+
+
+def test_nccl_communicator_without_gpu(lib):
+    """The data-parallel backward's NCCL layer (sd_comm_*): NCCL resolves at run
+    time, a unique id can be made without a GPU, and creating a communicator
+    without a B200 fails loudly (no CPU fallback)."""
+    import paper_2411_01238_b200 as sd
+
+    v = sd.Communicator.nccl_version()
+    assert v >= 22700, v  # NCCL >= 2.27
+    uid = sd.Communicator.new_unique_id()
+    assert len(uid) == 128 and uid != bytes(128)
+    if not _has_gpu():
+        with pytest.raises(RuntimeError):
+            sd.Communicator(1, 0, uid)
+    with pytest.raises(IndexError):
+        sd.Communicator(2, 2, uid)
+    assert lib.sd_layer_plan_backward_allreduce(None, None, 2, None, None) == _capi.SD_EINVAL
