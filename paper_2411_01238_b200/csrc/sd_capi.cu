@@ -192,7 +192,7 @@ void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed
 
 unsigned int* sched_slot(cudaStream_t s) {
     constexpr int kRing = 256;       // eager launches, round-robin
-    constexpr int kCaptured = 1024;  // launches captured into graphs, never reused
+    constexpr int kCaptured = 4096;  // launches captured into graphs, never reused (~10 KB each)
     static unsigned int* slots[64] = {nullptr};
     static std::atomic<uint32_t> next{0};
     static std::atomic<uint32_t> next_captured[64];
@@ -357,13 +357,13 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
     return encode_tmap(base, f32, 2, dims, strides, box);
 }
 
-CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld) {
+CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld, uint32_t atoms) {
     // view [red][mn] (mn contiguous, row pitch ld >= mn elements) as
-    // (64 mn_in, red, mn / 64 atoms): one box = two 64-wide SW128 atoms of 64
-    // reduction rows, atom-major in smem
+    // (64 mn_in, red, mn / 64 atoms): one box = `atoms` (2, or 1 for a half
+    // tile) 64-wide SW128 atoms of 64 reduction rows, atom-major in smem
     const cuuint64_t dims[3] = {64, red, mn / 64};
     const cuuint64_t strides[2] = {(ld ? ld : mn) * 2, 128};
-    const cuuint32_t box[3] = {64, 64, 2};
+    const cuuint32_t box[3] = {64, 64, atoms};
     return encode_tmap(base, false, 3, dims, strides, box);
 }
 

@@ -113,7 +113,7 @@ inline int gemm_units(const GemmArgs& a) {
 // CUDA graph gets a dedicated slot that is never handed out again (it is
 // replayed later, possibly beside eager launches).
 constexpr int kSchedWords = 64;
-constexpr int kTurnPerProb = 2048;
+constexpr int kTurnPerProb = 1216;  // split-K only below 2 x 148 narrow tiles: <= 295 tiles x 4 quarters
 constexpr int kTurnstiles = 2 * kTurnPerProb;
 constexpr int kSlotWords = kSchedWords + kTurnstiles;
 unsigned int* sched_slot(cudaStream_t s);
@@ -172,7 +172,7 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
                          uint32_t box_inner, uint32_t box_outer);
 // bf16 [red][mn] operand (mn contiguous, row pitch ld) as 3D (64, red, mn / 64): box = 128 mn
 // x 64 red in two atom-major 8 KB SW128 atoms; coordinates (0, red0, mn0 / 64).
-CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld);
+CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld, uint32_t atoms = 2);
 
 // ---------------------------------------------------------------- NCCL (sd_comm.cu)
 // In-place sum all-reduce of `count` elements (SD_DTYPE_*) on stream s.

@@ -305,3 +305,34 @@ def test_backward_waits_for_caller_pdl_kernel(sd, oracle):
         torch.cuda.synchronize()
         assert torch.equal(plan.dx, ref[0]), it
         assert torch.equal(plan.dw, ref[1]), it
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1, 0.5, 0.9])
+def test_graph_replay_equals_eager(sd, oracle, p):
+    """Layer steps captured into a CUDA graph (bench.py's timed region) and
+    replayed give the eager steps' outputs bit for bit: captured GEMM launches
+    get dedicated scheduler slots, the mask generation falls back to
+    griddepcontrol.wait under capture, split-K turnstiles reset themselves."""
+    M, N, K = 2048, 1536, 1024
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    plan = sd.LayerPlan(x, w, dy, p, dy_ready=True)
+    seeds = [3, 4, 5]
+    for sd_ in seeds:
+        plan.forward(sd_)
+        plan.backward()
+    torch.cuda.synchronize()
+    ref = [plan.y.clone(), plan.dx.clone(), plan.dw.clone(), plan.mask.words()]
+    gr = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(gr, stream=cs):
+        for sd_ in seeds:
+            plan.forward(sd_)
+            plan.backward()
+    for _ in range(3):
+        for t in (plan.y, plan.dx, plan.dw):
+            t.fill_(float("nan"))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(plan.y, ref[0]) and torch.equal(plan.dx, ref[1]) and torch.equal(plan.dw, ref[2])
+        assert plan.mask.words() == ref[3]
