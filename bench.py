@@ -457,7 +457,9 @@ def main():
         ms_dense_1cta = time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle)
     finally:
         _lib_t.sd_set_tuning(0)
-    ms_torch = time_steps(torch_step, args.steps, args.warmup)
+    # cuBLAS in ITS power-capped steady state too (a 0.3 s pre-roll left it ~15% faster than under sustained
+    # load, tools/ab_dense.py: 4096^3 cuBLAS and our 2-CTA dense step are within 1% when both are settled)
+    ms_torch = time_steps(torch_step, args.steps, args.warmup, preroll_s=settle)
 
     # ---- per-kernel durations at the headline p (roofline): each kernel run
     # back-to-back over the rotating input sets, one event pair around them
@@ -545,6 +547,7 @@ def main():
                 "executed_tflops": world * kp * flops_dense_step / (msp * 1e-3) / 1e12,
                 "speedup_vs_dense": ms_dense / msp,
                 "speedup_vs_dense_1cta": ms_dense_1cta / msp,
+                "speedup_vs_cublas": ms_torch / msp,
                 "time_vs_dense_over_keep": (msp / ms_dense) / max(kp, 1e-9),
             })
             if p != args.p:
@@ -578,7 +581,8 @@ def main():
                 t8["dense_tflops"] = 3 * 2 * S8 ** 3 / (msd8 * 1e-3) / 1e12
                 t8["speedup_vs_dense_p0.5"] = msd8 / ms8
             del pl8
-        mst = time_steps(lambda i: (x8 @ w8, x8.t() @ dy8, dy8 @ w8.t()), max(5, args.steps // 2), 3)
+        mst = time_steps(lambda i: (x8 @ w8, x8.t() @ dy8, dy8 @ w8.t()), max(5, args.steps // 2), 3,
+                         preroll_s=settle)
         t8["torch_cublas_dense_tflops"] = 3 * 2 * S8 ** 3 / (mst * 1e-3) / 1e12
         del x8, w8, dy8
         torch.cuda.empty_cache()
@@ -633,6 +637,7 @@ def main():
             "keep_fraction": keep, "executed_tflops": value * keep,
             "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
             "dense_1cta_ms_per_step": ms_dense_1cta, "speedup_vs_dense_1cta": ms_dense_1cta / ms,
+            "speedup_vs_cublas": ms_torch / ms,
             "dense_note": ("dense_ms_per_step: our 2-CTA (cta_group::2) dense kernel, the speed-up denominator; "
                            "dense_1cta_ms_per_step: the same dense step on the 1-CTA tiles the masked GEMMs use"),
             "isolated_ms_per_step": ms_isolated,

@@ -282,7 +282,9 @@ SD_API uint64_t sd_launch_count(void);
  *    blocks written as +0.0; bit-identical),
  * 2048 the masked 2-CTA dX reads its keep bits per output chunk and releases the
  *    mask workspace at exit (the path for CTAs with more than 512 units,
- *    forced here for tests).
+ *    forced here for tests),
+ * 4096 the 2-CTA kernel always uses 256x256 pair tiles, 8192 always 256x512
+ *    where the columns allow (default: 256x512 with at least two waves of them).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 

@@ -31,23 +31,37 @@
 namespace sd {
 namespace {
 
-constexpr int kStages2 = 6;
 constexpr int kHalfBytes = 128 * kBK * 2;  // 16 KB: one CTA's half of A or B per stage
 constexpr int kEpiWarps = 4;
 constexpr int kEpiBufBytes = 32 * 128;
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
-constexpr int kTile = 256;  // pair tile: 256 x 256
-
-constexpr int kOffA = 0;
-constexpr int kOffB = kOffA + kStages2 * kHalfBytes;
-constexpr int kOffEpi = kOffB + kStages2 * kHalfBytes;
-constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
-constexpr int kNumBars = 2 * kStages2 + 4;
-constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
-constexpr int kSmemBytes2 = kOffTmemSlot + 16 + 1024;
+constexpr int kTile = 256;  // pair tile rows (and columns of the narrow tile)
 constexpr int kMaxOwnUnits = 512;  // static smem: keep bits of a CTA's units (kFlagOutMask)
-static_assert(kSmemBytes2 + kMaxOwnUnits <= 232448, "shared memory budget (dynamic + static own_bits)");
+
+// Pair-tile shapes.
+//   narrow: 256 x 256 per pair, one M=256/N=256 MMA per K=16 step; each CTA
+//           ingests 32 KB per 64-deep stage for 2M MACs (16 KB / 1M); two
+//           256-column TMEM accumulators (tile i's epilogue overlaps tile i+1).
+//   WIDE:   256 x 512 per pair, two N=256 MMAs per K=16 step sharing the A
+//           tile; each CTA ingests 48 KB per stage for 4M MACs (12 KB / 1M, the
+//           shape cuBLAS uses for large bf16 GEMMs on this part: 256x256 per
+//           CTA, 4 x 48 KB stages). One 512-column accumulator whose two halves
+//           are released to the next tile one by one as the epilogue drains them.
+template <bool W>
+struct K2Cfg {
+    static constexpr int kStages = W ? 4 : 6;
+    static constexpr int kBSlots = W ? 2 : 1;  // 16 KB B boxes per stage per CTA
+    static constexpr int kTileN = W ? 512 : 256;
+    static constexpr int kOffA = 0;
+    static constexpr int kOffB = kOffA + kStages * kHalfBytes;
+    static constexpr int kOffEpi = kOffB + kStages * kBSlots * kHalfBytes;
+    static constexpr int kOffBar = kOffEpi + kEpiWarps * 2 * kEpiBufBytes;
+    static constexpr int kNumBars = 2 * kStages + 4;
+    static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
+    static constexpr int kSmem = kOffTmemSlot + 16 + 1024;
+    static_assert(kSmem + kMaxOwnUnits <= 232448, "shared memory budget (dynamic + static own_bits)");
+};
 
 __device__ __forceinline__ void tma_load_2sm_3d(const void* tmap, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
                                                 int32_t c2) {
@@ -93,19 +107,23 @@ struct Pair2Args {
     int own_cap;            // units whose keep bits are read up front (<= kMaxOwnUnits; 0: per chunk)
 };
 
+template <bool W>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     sd_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmOut, const Pair2Args P) {
+    using C = K2Cfg<W>;
+    constexpr int kStages2 = C::kStages;
+    constexpr int kTileN = C::kTileN;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
     const uint32_t sbase = ptx::smem_u32(smem);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     uint64_t* full_bar = bars;               // leader only
     uint64_t* empty_bar = bars + kStages2;   // each CTA
     uint64_t* tfull_bar = bars + 2 * kStages2;
     uint64_t* tempty_bar = bars + 2 * kStages2 + 2;  // leader only
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmemSlot);
 
     const GemmArgs& a = P.g;
     const uint32_t warp = threadIdx.x / 32;
@@ -113,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const bool a_mn = a.flags & kFlagAMN, b_mn = a.flags & kFlagBMN, f32 = a.flags & kFlagF32;
-    const bool unioned = P.pair_cnt != nullptr;
+    const bool unioned = !W && P.pair_cnt != nullptr;
     const int num_units = P.n_pair_rows * P.n_col_tiles;
     const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
 
@@ -156,8 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         prow = g * G + (rem - ct * rows_in_group);
     };
 
-    // kFlagOutMask: this CTA's keep bits (its 128-row block x the tile's two
-    // 128-column blocks) for every unit it will run, read once up front, so the
+    // kFlagOutMask: this CTA's keep bits (its 128-row block x the tile's two or
+    // four 128-column blocks) for every unit it will run, read once up front, so the
     // mask workspace is released now instead of at exit and the next mask
     // generation overlaps this grid (more than kMaxOwnUnits units: at exit)
     __shared__ uint8_t own_bits[kMaxOwnUnits];
@@ -167,10 +185,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         for (int k = threadIdx.x; k < own_units; k += kThreads) {
             int prow, ct;
             decode(cluster_id + k * n_clusters, prow, ct);
-            const int64_t bit = static_cast<int64_t>(2 * prow + static_cast<int>(rank)) * a.mask_cols + 2 * ct;
-            const uint64_t w0 = __ldcg(a.words + (bit >> 6));
-            const uint64_t w1 = __ldcg(a.words + ((bit + 1) >> 6));
-            own_bits[k] = static_cast<uint8_t>(((w0 >> (bit & 63)) & 1ull) | (((w1 >> ((bit + 1) & 63)) & 1ull) << 1));
+            constexpr int nb = kTileN / 128;
+            const int64_t bit = static_cast<int64_t>(2 * prow + static_cast<int>(rank)) * a.mask_cols + nb * ct;
+            uint32_t v = 0;
+#pragma unroll
+            for (int j = 0; j < nb; ++j) v |= static_cast<uint32_t>((__ldcg(a.words + ((bit + j) >> 6)) >> ((bit + j) & 63)) & 1ull) << j;
+            own_bits[k] = static_cast<uint8_t>(v);
         }
         __syncthreads();
         if (P.release && threadIdx.x == 0) {
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 decode(u, prow, ct);
                 const int nst = unit_stages(prow);
                 const int row0 = prow * kTile + 128 * static_cast<int>(rank);  // this CTA's A rows
-                const int col0 = ct * kTile + 128 * static_cast<int>(rank);    // this CTA's B columns
+                const int col0 = ct * kTileN + 128 * static_cast<int>(rank);   // this CTA's B columns (per 256)
                 const int spb = a.red_blk / kBK;
                 const int32_t* lst = unioned ? P.pair_idx + static_cast<int64_t>(prow) * P.pair_stride : nullptr;
                 int entry = 0;
@@ -208,11 +228,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                         r0 = s * kBK;
                     }
                     ptx::mbar_wait(empty_bar + stage, phase ^ 1);
-                    uint8_t* sA = smem + kOffA + stage * kHalfBytes;
-                    uint8_t* sB = smem + kOffB + stage * kHalfBytes;
+                    uint8_t* sA = smem + C::kOffA + stage * kHalfBytes;
+                    uint8_t* sB = smem + C::kOffB + stage * C::kBSlots * kHalfBytes;
                     if (leader) {
                         // both CTAs' A and B halves (a dropped A half is a zero-filled box, same bytes)
-                        ptx::mbar_arrive_expect_tx(full_bar + stage, 4 * kHalfBytes);
+                        ptx::mbar_arrive_expect_tx(full_bar + stage, (2 + 2 * C::kBSlots) * kHalfBytes);
                     } else {
                         ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(full_bar + stage), 0));
                     }
@@ -224,10 +244,13 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                     } else {
                         tma_load_2sm_3d(&tmA, full_bar + stage, sA, 0, r0, arow / 64);
                     }
-                    if (!b_mn) {
-                        tma_load_2sm(&tmB, full_bar + stage, sB, r0, col0);
-                    } else {
-                        tma_load_2sm_3d(&tmB, full_bar + stage, sB, 0, r0, col0 / 64);
+#pragma unroll
+                    for (int j = 0; j < C::kBSlots; ++j) {
+                        if (!b_mn) {
+                            tma_load_2sm(&tmB, full_bar + stage, sB + j * kHalfBytes, r0, col0 + 256 * j);
+                        } else {
+                            tma_load_2sm_3d(&tmB, full_bar + stage, sB + j * kHalfBytes, 0, r0, (col0 + 256 * j) / 64);
+                        }
                     }
                     if (++stage == kStages2) {
                         stage = 0;
@@ -250,37 +273,74 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 decode(u, prow, ct);
                 const int nst = unit_stages(prow);
                 if (nst == 0) continue;
-                const uint32_t acc = acc_iter & 1;
-                const uint32_t acc_phase = (acc_iter >> 1) & 1;
-                ++acc_iter;
-                ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * kTile;
-                for (int s = 0; s < nst; ++s) {
-                    ptx::mbar_wait(full_bar + stage, phase);
+                if constexpr (!W) {
+                    const uint32_t acc = acc_iter & 1;
+                    const uint32_t acc_phase = (acc_iter >> 1) & 1;
+                    ++acc_iter;
+                    ptx::mbar_wait(tempty_bar + acc, acc_phase ^ 1);
                     ptx::tc_fence_after();
-                    const uint32_t a_addr = sbase + kOffA + stage * kHalfBytes;
-                    const uint32_t b_addr = sbase + kOffB + stage * kHalfBytes;
+                    const uint32_t d_tmem = tmem_base + acc * kTile;
+                    for (int s = 0; s < nst; ++s) {
+                        ptx::mbar_wait(full_bar + stage, phase);
+                        ptx::tc_fence_after();
+                        const uint32_t a_addr = sbase + C::kOffA + stage * kHalfBytes;
+                        const uint32_t b_addr = sbase + C::kOffB + stage * kHalfBytes;
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
-                        const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
-                        mma2_bf16(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                            const uint64_t bd = ptx::make_sw128_desc(b_addr + k * b_step, b_lbo, 1024);
+                            mma2_bf16(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                        }
+                        commit2_mc(empty_bar + stage, 0x3);
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
-                    commit2_mc(empty_bar + stage, 0x3);
-                    if (++stage == kStages2) {
-                        stage = 0;
-                        phase ^= 1;
+                    commit2_mc(tfull_bar + acc, 0x3);
+                } else {
+                    // one 512-column accumulator, half h = TMEM columns [256h, 256h + 256):
+                    // half 0 is free once the previous tile's epilogue drained it
+                    // (tempty[0]), half 1 likewise (tempty[1]) — waited for only
+                    // before the first MMA into it
+                    const uint32_t rphase = acc_iter & 1;
+                    ++acc_iter;
+                    ptx::mbar_wait(tempty_bar + 0, rphase ^ 1);
+                    ptx::tc_fence_after();
+                    for (int s = 0; s < nst; ++s) {
+                        ptx::mbar_wait(full_bar + stage, phase);
+                        ptx::tc_fence_after();
+                        const uint32_t a_addr = sbase + C::kOffA + stage * kHalfBytes;
+                        const uint32_t b_addr = sbase + C::kOffB + stage * 2 * kHalfBytes;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (h == 1 && s == 0) {
+                                ptx::mbar_wait(tempty_bar + 1, rphase ^ 1);
+                                ptx::tc_fence_after();
+                            }
+#pragma unroll
+                            for (int k = 0; k < kBK / 16; ++k) {
+                                const uint64_t ad = ptx::make_sw128_desc(a_addr + k * a_step, a_lbo, 1024);
+                                const uint64_t bd =
+                                    ptx::make_sw128_desc(b_addr + h * kHalfBytes + k * b_step, b_lbo, 1024);
+                                mma2_bf16(tmem_base + 256 * h, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                            }
+                        }
+                        commit2_mc(empty_bar + stage, 0x3);
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
+                    commit2_mc(tfull_bar + 0, 0x3);
                 }
-                commit2_mc(tfull_bar + acc, 0x3);
             }
         }
     } else if (warp >= 4) {
         // ===================== epilogue (both CTAs, own 128 rows) =====================
         const uint32_t q = warp & 3;
-        uint8_t* ebuf = smem + kOffEpi + q * 2 * kEpiBufBytes;
-        const uint32_t ebuf_addr = sbase + kOffEpi + q * 2 * kEpiBufBytes;
+        uint8_t* ebuf = smem + C::kOffEpi + q * 2 * kEpiBufBytes;
+        const uint32_t ebuf_addr = sbase + C::kOffEpi + q * 2 * kEpiBufBytes;
         uint32_t bi = 0, acc_iter = 0;
         const int chunk = f32 ? 32 : 64;
         const int esz = f32 ? 4 : 2;
@@ -299,12 +359,13 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 }
                 continue;
             }
-            const uint32_t acc = acc_iter & 1;
-            const uint32_t acc_phase = (acc_iter >> 1) & 1;
+            // narrow: accumulator (acc_iter & 1); WIDE: the one 512-column accumulator
+            const uint32_t acc = W ? 0u : (acc_iter & 1);
+            const uint32_t acc_phase = W ? (acc_iter & 1) : ((acc_iter >> 1) & 1);
             ++acc_iter;
             ptx::mbar_wait(tfull_bar + acc, acc_phase);
             ptx::tc_fence_after();
-            const int nchunks = kTile / chunk;
+            const int nchunks = kTileN / chunk;
             for (int c = 0; c < nchunks; ++c) {
                 const uint32_t taddr = tmem_base + ((32 * q) << 16) + acc * kTile + c * chunk;
                 uint32_t v[64];
@@ -318,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                     if (bits_up_front) {
                         kept = (own_bits[(u - cluster_id) / n_clusters] >> cb) & 1u;
                     } else {
-                        const int64_t bit = static_cast<int64_t>(row_first / 128) * a.mask_cols + 2 * ct + cb;
+                        const int64_t bit =
+                            static_cast<int64_t>(row_first / 128) * a.mask_cols + (kTileN / 128) * ct + cb;
                         kept = (__ldcg(a.words + (bit >> 6)) >> (bit & 63)) & 1ull;
                     }
                     if (!kept) {
@@ -326,10 +388,21 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                         for (int j = 0; j < 64; ++j) v[j] = 0u;
                     }
                 }
-                if (c == nchunks - 1) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(tempty_bar + acc), 0));
+                if constexpr (!W) {
+                    if (c == nchunks - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(tempty_bar + acc), 0));
+                    }
+                } else {
+                    // half 0 drained: the next tile's MMAs may start on it
+                    const bool end_h0 = (c + 1) * chunk == 256, end_h1 = c == nchunks - 1;
+                    if (end_h0 || end_h1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(tempty_bar + (end_h0 ? 0 : 1)), 0));
+                    }
                 }
                 if (lane == 0) ptx::bulk_wait_group_read<1>();
                 __syncwarp();
@@ -354,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, ct * kTile + c * chunk, row_first);
+                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, ct * kTileN + c * chunk, row_first);
                     ptx::bulk_commit_group();
                 }
                 bi ^= 1;
@@ -390,14 +463,25 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
                   bool no_wait, unsigned int* release) {
     configure_once_per_device(1, [] {
-        check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2),
+        check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        K2Cfg<false>::kSmem),
                    "cudaFuncSetAttribute(gemm2 smem)");
+        check_cuda(cudaFuncSetAttribute(sd_gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        K2Cfg<true>::kSmem),
+                   "cudaFuncSetAttribute(gemm2 wide smem)");
     });
+    // 256 x 512 pair tiles (12 KB of operands per 1M MACs instead of 16) when
+    // the columns allow it and there are at least two waves of them
+    const int sms = num_sms();
+    const int wide_units = (g.rows_out / 256) * (g.cols_out / 512);
+    bool wide = !pair_cnt && g.cols_out % 512 == 0 && wide_units >= sms;
+    if (tuning() & kTuneGemm2Narrow) wide = false;
+    if ((tuning() & kTuneGemm2Wide) && !pair_cnt && g.cols_out % 512 == 0) wide = true;
     Pair2Args P;
     std::memset(&P, 0, sizeof P);
     P.g = g;
     P.n_pair_rows = g.rows_out / 256;
-    P.n_col_tiles = g.cols_out / 256;
+    P.n_col_tiles = g.cols_out / (wide ? 512 : 256);
     P.pair_cnt = pair_cnt;
     P.pair_idx = pair_idx;
     P.pair_stride = pair_stride;
@@ -405,19 +489,20 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     P.release = release;
     P.own_cap = (tuning() & kTuneNoOwnBits) ? 0 : kMaxOwnUnits;
     const int units = P.n_pair_rows * P.n_col_tiles;
-    int clusters = std::min(units, num_sms() / 2);
+    int clusters = std::min(units, sms / 2);
     if (clusters <= 0) return;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes2;
+    cfg.dynamicSmemBytes = wide ? K2Cfg<true>::kSmem : K2Cfg<false>::kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel, ta, tb, tout, P), "sd_gemm2_kernel launch");
+    if (wide) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel<true>, ta, tb, tout, P), "sd_gemm2_kernel<wide> launch");
+    else check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm2_kernel<false>, ta, tb, tout, P), "sd_gemm2_kernel launch");
     note_launch();
     if (release) mask_note_readers(release, static_cast<int>(cfg.gridDim.x), s);
     // this kernel does not release mask workspaces: a following generation

@@ -138,6 +138,8 @@ enum TuneFlags : int {
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
     kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
     kTuneNoMaskedDense = 1024,   // low-p dX stays on the sdd kernel instead of the masked 2-CTA dense GEMM
+    kTuneGemm2Narrow = 4096,     // 2-CTA kernel: always 256 x 256 pair tiles
+    kTuneGemm2Wide = 8192,       // 2-CTA kernel: 256 x 512 pair tiles whenever the columns allow
     kTuneNoOwnBits = 2048,       // masked 2-CTA dX reads keep bits per chunk and releases at exit (the
                                  // > kMaxOwnUnits fallback, forced for tests)
 };

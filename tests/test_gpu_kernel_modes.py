@@ -336,3 +336,53 @@ def test_graph_replay_equals_eager(sd, oracle, p):
         torch.cuda.synchronize()
         assert torch.equal(plan.y, ref[0]) and torch.equal(plan.dx, ref[1]) and torch.equal(plan.dw, ref[2])
         assert plan.mask.words() == ref[3]
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 2048, 768), (2048, 1024, 1536)])
+@pytest.mark.parametrize("layout", ["nn", "nt", "tn"])
+@pytest.mark.parametrize("out_f32", [True, False])
+def test_gemm2_wide_equals_narrow_bitwise(sd, oracle, M, N, K, layout, out_f32):
+    """2-CTA pair tiles 256 x 512 (two N=256 MMAs per A tile, tuning 8192) vs
+    256 x 256 (tuning 4096): same bits for every layout of the dense GEMMs
+    (forward nn, dX nt, dW tn) — each element reduced over the same K=16 steps."""
+    lib = sd.load_library()
+    a_mn, b_mn = {"nn": (0, 1), "nt": (0, 0), "tn": (1, 1)}[layout]
+    a = _dev(oracle, K, M, 1) if a_mn else _dev(oracle, M, K, 1)
+    b = _dev(oracle, K, N, 2) if b_mn else _dev(oracle, N, K, 2)
+    dt, tdt = (0, torch.float32) if out_f32 else (1, torch.bfloat16)
+    outs = []
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    try:
+        for bits in (4096, 8192, 16):
+            lib.sd_set_tuning(bits)
+            c = torch.full((M, N), float("nan"), dtype=tdt, device="cuda")
+            sd.api.check(lib.sd_gemm_ex(a.data_ptr(), a_mn, b.data_ptr(), b_mn, c.data_ptr(), dt, M, N, K, 1.5, st))
+            torch.cuda.synchronize()
+            outs.append(c)
+    finally:
+        lib.sd_set_tuning(0)
+    assert torch.equal(outs[0], outs[1])  # 2-CTA narrow == wide
+    assert torch.equal(outs[0], outs[2])  # == the 1-CTA kernel
+    assert not torch.isnan(outs[0].float()).any()
+
+
+@pytest.mark.parametrize("p", [0.1, 0.3])
+def test_masked_dense_dx_wide_pairs_bitwise(sd, oracle, p):
+    """The masked 2-CTA dX on 256 x 512 pair tiles (four 128-column keep bits per
+    unit) equals the sdd kernel bit for bit; also with per-chunk bit reads."""
+    lib = sd.load_library()
+    M, N, K = 2048, 1024, 2048
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    outs = []
+    try:
+        for bits in (8192, 8192 | 2048, 1024):
+            lib.sd_set_tuning(bits)
+            plan = sd.LayerPlan(x, w, dy, p)
+            plan.forward(11)
+            plan.backward_dx()
+            torch.cuda.synchronize()
+            outs.append(plan.dx.clone())
+    finally:
+        lib.sd_set_tuning(0)
+    assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
+    assert torch.equal(outs[1].view(torch.int16), outs[2].view(torch.int16))

@@ -1,5 +1,6 @@
 """Launch a fixed set of kernels once each (after warm-up) for ncu capture (dev tool).
-python tools/prof_kernels.py SIZE P [which...]   which in {fwd, dw, dx, dense_nn, dense_nt, dense_tn, mask}"""
+python tools/prof_kernels.py SIZE P [which...]   which in {fwd, dw, dx, dense_nn, dense_nt, dense_tn, mask, bwd,
+cublas_nn}"""
 import ctypes
 import sys
 
@@ -38,6 +39,7 @@ fns = {
     "dense_tn": lambda: lib.sd_dense_gemm_tn(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, K, N, M, st()),
     "mask": lambda: sd.sample_mask(sd.DropoutSpec(P, 128, 128, 1), M, K, out=m),
     "bwd": lambda: plan.backward(),
+    "cublas_nn": lambda: torch.matmul(x, w, out=y),
 }
 def run(k):
     r = fns[k]()
