@@ -284,7 +284,10 @@ SD_API uint64_t sd_launch_count(void);
  *    mask workspace at exit (the path for CTAs with more than 512 units,
  *    forced here for tests),
  * 4096 the 2-CTA kernel always uses 256x256 pair tiles, 8192 always 256x512
- *    where the columns allow (default: 256x512 with at least two waves of them).
+ *    where the columns allow (default: 256x512 with at least two waves of them),
+ * 16384 a plan with 0.3 < p <= 0.7 splits dX by mask-row pairs: the column
+ *    blocks both rows of a pair keep run on the 2-CTA kernel, the rest on the
+ *    1-CTA sdd kernel (bit-identical; off by default: not faster, measured).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 

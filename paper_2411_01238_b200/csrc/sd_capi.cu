@@ -723,6 +723,11 @@ struct sd_layer_plan {
     // order as in the sdd kernel: bit-identical)
     sd::GemmCall dx_masked;
     bool dx_masked_ok = false;
+    // mid p: dX split by mask-row pairs (sd_gemm2.cu kFlagPairs): the column
+    // blocks both rows of a pair keep on the 2-CTA kernel, the remainder and
+    // the zero fill on the 1-CTA sdd kernel (bit-identical to the plain sdd)
+    sd::GemmCall dx_pairs, dx_rem;
+    bool pairs_ok = false;
     // data-parallel backward (sd_layer_plan_backward_allreduce): one event per
     // dW slab (compute -> comm stream) and one for the last all-reduce
     std::vector<cudaEvent_t> slab_done;
@@ -735,6 +740,7 @@ struct sd_layer_plan {
 
 namespace {
 constexpr double kMaskedDenseMaxP = 0.3;
+constexpr double kPairsMaxP = 0.7;  // above: too few common kept blocks per row pair to pay a launch
 
 // Measured (tools/ab_steps.py, profiles/r01_masked_dx_ab.txt): at 4096^3 the
 // split backward gains 1-2% at p <= 0.2 and loses 3% at p = 0.3 (the fused
@@ -746,6 +752,18 @@ bool use_masked_dx(const sd_layer_plan* plan) {
         return false;
     const int64_t tiles = static_cast<int64_t>(plan->dx_masked.args.rows_out / 256) * (plan->dx_masked.args.cols_out / 256);
     return plan->p <= 0.2 || tiles >= 4 * static_cast<int64_t>(sd::num_sms());
+}
+
+bool use_pairs(const sd_layer_plan* plan) {
+    return plan->pairs_ok && (sd::tuning() & sd::kTunePairs) && plan->p > 0.0 && plan->p <= kPairsMaxP &&
+           !use_masked_dx(plan);
+}
+
+// dX of a mid-p plan: the row-pair 2-CTA part, then (never waiting for it: the
+// output blocks are disjoint) the 1-CTA remainder (+ dW when fused).
+void launch_dx_pairs(const sd_layer_plan* plan, cudaStream_t s, bool no_wait) {
+    const sd::GemmCall& g = plan->dx_pairs;
+    sd::launch_gemm2(g.ta, g.tb, g.tout, g.args, nullptr, nullptr, 0, s, no_wait, g.release);
 }
 
 // The backward reads X, W, dY and the mask lists and writes dX, dW; the forward
@@ -946,6 +964,21 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dx_masked.release = mask_release_counter(mask);
         tmp.dx_masked_ok = p <= kMaskedDenseMaxP && mask->m_blk == 128 && mask->k_blk == 128 &&
                            gemm2_supported(tmp.dx_masked.args);
+        // row-pair split of dX: A = dY (K-major), B = W (K-major, read in place)
+        tmp.dx_pairs.ta = tmp.dx.ta;
+        tmp.dx_pairs.tb = tmp.dx.tb;
+        tmp.dx_pairs.tout = tmp.dx.tout;
+        tmp.dx_pairs.args = base_args(m, k, n, s, dx);
+        tmp.dx_pairs.args.flags = kFlagPairs | (dx_dtype == SD_DTYPE_F32 ? kFlagF32 : 0u);
+        tmp.dx_pairs.args.words = mask->words;
+        tmp.dx_pairs.args.mask_cols = mask->block_cols;
+        tmp.dx_pairs.args.out_row_blk = mask->m_blk;
+        tmp.dx_pairs.args.out_col_blk = mask->k_blk;
+        tmp.dx_pairs.release = mask_release_counter(mask);
+        tmp.dx_rem = tmp.dx;
+        tmp.dx_rem.args.flags |= kFlagPairs;
+        tmp.pairs_ok = mask->m_blk == 128 && mask->k_blk == 128 && mask->block_rows % 2 == 0 &&
+                       gemm2_pairs_supported(tmp.dx_pairs.args);
         // the early backward relies on the forward writing nothing the backward
         // touches: with Y overlapping X, W, dY, dX or dW, or the mask workspace
         // overlapping any buffer, every backward waits for the forward grid
@@ -1045,7 +1078,12 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
                                f32 ? SD_DTYPE_F32 : SD_DTYPE_BF16, cs);
             (void)el;
         }
-        launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, s);
+        if (use_pairs(plan)) {
+            launch_dx_pairs(plan, s, false);
+            launch_gemm(plan->dx_rem, s, true);
+        } else {
+            launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, s);
+        }
         if (cs != s) {
             check_cuda(cudaEventRecord(plan->reduced, cs), "cudaEventRecord(all-reduce)");
             check_cuda(cudaStreamWaitEvent(s, plan->reduced, 0), "cudaStreamWaitEvent(all-reduce)");
@@ -1056,8 +1094,13 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
 int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, as_stream(stream),
-                    take_no_wait(plan, as_stream(stream)));
+        const bool nw = take_no_wait(plan, as_stream(stream));
+        if (use_pairs(plan)) {
+            launch_dx_pairs(plan, as_stream(stream), nw);
+            launch_gemm(plan->dx_rem, as_stream(stream), true);
+        } else {
+            launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, as_stream(stream), nw);
+        }
     });
 }
 
@@ -1072,6 +1115,11 @@ int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
             // launches, the second never waits for the first
             launch_gemm(plan->dw, as_stream(stream), nw);
             launch_gemm(plan->dx_masked, as_stream(stream), true);
+        } else if (use_pairs(plan)) {
+            // dX's row-pair part on the 2-CTA kernel, then dX's remainder and dW
+            // as one 1-CTA launch that fills the SMs the first one leaves
+            launch_dx_pairs(plan, as_stream(stream), nw);
+            fused_backward(plan->dx_rem, plan->dw, as_stream(stream), true);
         } else {
             fused_backward(plan->dx, plan->dw, as_stream(stream), nw);
         }

@@ -180,6 +180,15 @@ struct TensorMaps {
     CUtensorMap m[3 * kMaxProblems];  // A, B, Out per problem
 };
 
+// Bits of mask row r (C <= 64 columns), row-major LSB-first words.
+__device__ __forceinline__ uint64_t pair_row_bits(const uint64_t* words, int r, int C) {
+    const int64_t b = static_cast<int64_t>(r) * C;
+    const int sh = static_cast<int>(b & 63);
+    uint64_t v = __ldcg(words + (b >> 6)) >> sh;
+    if (sh + C > 64) v |= __ldcg(words + (b >> 6) + 1) << (64 - sh);
+    return C == 64 ? v : (v & ((1ull << C) - 1));
+}
+
 template <bool WIDE>
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) {
     Unit t;
@@ -244,10 +253,31 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
         const int ndrop = a.mask_cols - cnt;
         const int32_t* row = a.list_idx + static_cast<int64_t>(t.list_row) * a.list_stride;
         t.n0 = 0;
-        for (int j = 0; j < per_unit; ++j) {
-            const int li = cu * per_unit + j;
-            if (li < cnt) t.slot_blk[t.nslots++] = __ldcg(row + li);
-            if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
+        if (a.flags & kFlagPairs) {
+            // row-pair split (sd_gemm2.cu): the column blocks this row and its
+            // pair partner both keep, taken in ascending pairs, are the 2-CTA
+            // kernel's; this unit packs the REMAINING kept blocks (and zero-fills
+            // the dropped ones from the list tail as usual)
+            const uint64_t mine = pair_row_bits(a.words, t.list_row, a.mask_cols);
+            const uint64_t common = mine & pair_row_bits(a.words, t.list_row ^ 1, a.mask_cols);
+            uint64_t paired = common;
+            for (int i = __popcll(common) & ~1; i < __popcll(common); ++i) paired &= ~(1ull << (63 - __clzll(paired)));
+            uint64_t rem = mine & ~paired;
+            for (int i = 0; i < cu * per_unit && rem; ++i) rem &= rem - 1;  // skip earlier units' blocks
+            for (int j = 0; j < per_unit; ++j) {
+                const int li = cu * per_unit + j;
+                if (rem) {
+                    t.slot_blk[t.nslots++] = __ffsll(static_cast<long long>(rem)) - 1;
+                    rem &= rem - 1;
+                }
+                if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
+            }
+        } else {
+            for (int j = 0; j < per_unit; ++j) {
+                const int li = cu * per_unit + j;
+                if (li < cnt) t.slot_blk[t.nslots++] = __ldcg(row + li);
+                if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
+            }
         }
         t.n_eff = t.nslots * a.out_col_blk;
         t.nstages = a.red / kBK;

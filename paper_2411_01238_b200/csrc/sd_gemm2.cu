@@ -12,6 +12,17 @@
 //   empty barrier   each CTA; the leader's commit multicasts to both
 //   TMEM full       each CTA; the leader's commit multicasts to both
 //   TMEM empty      leader only; all 8 epilogue warps of the pair arrive
+// Row-pair (biclique) sdd mode, kFlagPairs (the dX of a layer at mid p): for
+// 128-row mask rows 2i and 2i+1, the output column blocks BOTH keep are taken in
+// ascending pairs (c_a, c_b); each pair is one 256 x 256 unit — CTA 0 computes
+// rows 2i, CTA 1 rows 2i+1, both over B = W rows of blocks c_a (CTA 0's half)
+// and c_b (CTA 1's half) — so a fraction (1-p) of dX's kept work runs at the
+// pair's 16 KB of operands per 1M MACs instead of the 1-CTA sdd tile's 24 KB.
+// The remaining kept blocks (and the zero fill of the dropped ones) are the
+// 1-CTA sdd kernel's (sd_gemm.cu, kFlagPairs: remainder lists). Units are
+// enumerated from the mask words on the fly (pair_walk below). Every kept
+// block is reduced over the same 64-deep stages in the same order as in the
+// 1-CTA kernel: bit-identical.
 // Union mode (dsd with a list per 128-row block): the pair's two row blocks
 // walk the UNION of their kept lists; a CTA whose own row dropped a block
 // loads an all-out-of-bounds box instead (TMA zero fill, no memory traffic), so
@@ -94,6 +105,40 @@ __device__ __forceinline__ void commit2_mc(uint64_t* bar, uint16_t mask) {
                  : "memory");
 }
 
+// Bits of mask row r (C <= 64 columns, bit c = column c), row-major LSB-first words.
+__device__ __forceinline__ uint64_t row_bits(const uint64_t* words, int r, int C) {
+    const int64_t b = static_cast<int64_t>(r) * C;
+    const int sh = static_cast<int>(b & 63);
+    uint64_t v = __ldcg(words + (b >> 6)) >> sh;
+    if (sh + C > 64) v |= __ldcg(words + (b >> 6) + 1) << (64 - sh);
+    return C == 64 ? v : (v & ((1ull << C) - 1));
+}
+// index of the n-th (0-based) set bit of v (v has more than n set bits)
+__device__ __forceinline__ int nth_set_bit(uint64_t v, int n) {
+    for (int i = 0; i < n; ++i) v &= v - 1;
+    return __ffsll(static_cast<long long>(v)) - 1;
+}
+
+// Enumerates the row-pair units in order: unit u lies in pair row `row`, as its
+// (u - base)-th pair of common kept columns. Walkers only move forward.
+struct PairWalk {
+    int row = 0, base = 0, cnt = -1;
+    uint64_t common = 0;
+};
+__device__ __forceinline__ bool pair_walk(PairWalk& w, int u, const uint64_t* words, int n_pair_rows, int C) {
+    while (w.row < n_pair_rows) {
+        if (w.cnt < 0) {
+            w.common = row_bits(words, 2 * w.row, C) & row_bits(words, 2 * w.row + 1, C);
+            w.cnt = __popcll(w.common) / 2;
+        }
+        if (u < w.base + w.cnt) return true;
+        w.base += w.cnt;
+        ++w.row;
+        w.cnt = -1;
+    }
+    return false;
+}
+
 struct Pair2Args {
     GemmArgs g;         // rows_out, cols_out, red, flags (kFlagAMN/BMN/F32), scale, out, list*, red_blk, out_row_blk
     int n_pair_rows;    // rows_out / 256
@@ -132,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const bool leader = rank == 0;
     const bool a_mn = a.flags & kFlagAMN, b_mn = a.flags & kFlagBMN, f32 = a.flags & kFlagF32;
     const bool unioned = !W && P.pair_cnt != nullptr;
+    const bool pairs = !W && (a.flags & kFlagPairs);  // row-pair sdd units (dX)
     const int num_units = P.n_pair_rows * P.n_col_tiles;
     const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
 
@@ -180,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     // generation overlaps this grid (more than kMaxOwnUnits units: at exit)
     __shared__ uint8_t own_bits[kMaxOwnUnits];
     const int own_units = (num_units - cluster_id + n_clusters - 1) / n_clusters;
-    const bool bits_up_front = (a.flags & kFlagOutMask) && own_units <= P.own_cap;
+    const bool bits_up_front = !pairs && (a.flags & kFlagOutMask) && own_units <= P.own_cap;
     if (bits_up_front) {
         for (int k = threadIdx.x; k < own_units; k += kThreads) {
             int prow, ct;
@@ -202,18 +248,37 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         if (unioned) return __ldg(P.pair_cnt + prow) * (a.red_blk / kBK);
         return a.red / kBK;
     };
+    // next unit of this cluster: u -> pair row, column tile (dense/union) or the
+    // two 128-column output blocks (row-pair mode); false past the last unit
+    auto next_unit = [&](PairWalk& wk, int u, int& prow, int& ct, int& ca, int& cb) -> bool {
+        if (!pairs) {
+            if (u >= num_units) return false;
+            decode(u, prow, ct);
+            ca = 2 * ct;
+            cb = 2 * ct + 1;
+            return true;
+        }
+        if (!pair_walk(wk, u, a.words, P.n_pair_rows, a.mask_cols)) return false;
+        prow = wk.row;
+        ct = 0;
+        const int j = u - wk.base;
+        ca = nth_set_bit(wk.common, 2 * j);
+        cb = nth_set_bit(wk.common, 2 * j + 1);
+        return true;
+    };
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = cluster_id; u < num_units; u += n_clusters) {
-                int prow, ct;
-                decode(u, prow, ct);
+            PairWalk wk;
+            int prow, ct, ca, cb;
+            for (int u = cluster_id; next_unit(wk, u, prow, ct, ca, cb); u += n_clusters) {
                 const int nst = unit_stages(prow);
                 const int row0 = prow * kTile + 128 * static_cast<int>(rank);  // this CTA's A rows
-                const int col0 = ct * kTileN + 128 * static_cast<int>(rank);   // this CTA's B columns (per 256)
+                // this CTA's B columns (per 256); row-pair mode: its output column block
+                const int col0 = pairs ? (rank ? cb : ca) * 128 : ct * kTileN + 128 * static_cast<int>(rank);
                 const int spb = a.red_blk / kBK;
                 const int32_t* lst = unioned ? P.pair_idx + static_cast<int64_t>(prow) * P.pair_stride : nullptr;
                 int entry = 0;
@@ -268,9 +333,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             const uint32_t idesc = ptx::make_idesc_bf16(256, 256, a_mn, b_mn);
             const uint32_t a_step = a_mn ? 2048u : 32u, b_step = b_mn ? 2048u : 32u;
             const uint32_t a_lbo = a_mn ? 8192u : 0u, b_lbo = b_mn ? 8192u : 0u;
-            for (int u = cluster_id; u < num_units; u += n_clusters) {
-                int prow, ct;
-                decode(u, prow, ct);
+            PairWalk wk;
+            int prow, ct, ca, cb;
+            for (int u = cluster_id; next_unit(wk, u, prow, ct, ca, cb); u += n_clusters) {
                 const int nst = unit_stages(prow);
                 if (nst == 0) continue;
                 if constexpr (!W) {
@@ -344,9 +409,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         uint32_t bi = 0, acc_iter = 0;
         const int chunk = f32 ? 32 : 64;
         const int esz = f32 ? 4 : 2;
-        for (int u = cluster_id; u < num_units; u += n_clusters) {
-            int prow, ct;
-            decode(u, prow, ct);
+        PairWalk wk;
+        int prow, ct, ca, cb;
+        for (int u = cluster_id; next_unit(wk, u, prow, ct, ca, cb); u += n_clusters) {
             const int row_first = prow * kTile + 128 * static_cast<int>(rank) + 32 * q;
             if (unit_stages(prow) == 0) {
                 // both rows of the pair fully dropped: exact zeros
@@ -427,7 +492,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, ct * kTileN + c * chunk, row_first);
+                    // row-pair mode: columns [0,128) of the unit are block ca, [128,256) block cb
+                    const int col = pairs ? (c * chunk < 128 ? ca * 128 + c * chunk : cb * 128 + c * chunk - 128)
+                                          : ct * kTileN + c * chunk;
+                    ptx::tma_store_2d(&tmOut, ebuf + bi * kEpiBufBytes, col, row_first);
                     ptx::bulk_commit_group();
                 }
                 bi ^= 1;
@@ -459,6 +527,12 @@ bool gemm2_supported(const GemmArgs& a) {
            a.red % kBK == 0;
 }
 
+bool gemm2_pairs_supported(const GemmArgs& a) {
+    return !(a.flags & (kFlagSDD | kFlagReduce)) && a.rows_out % 256 == 0 && a.red % kBK == 0 &&
+           a.out_row_blk == 128 && a.out_col_blk == 128 && a.mask_cols >= 2 && a.mask_cols <= 64 &&
+           a.cols_out == 128 * a.mask_cols && a.words != nullptr;
+}
+
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
                   bool no_wait, unsigned int* release) {
@@ -474,9 +548,10 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     // the columns allow it and there are at least two waves of them
     const int sms = num_sms();
     const int wide_units = (g.rows_out / 256) * (g.cols_out / 512);
-    bool wide = !pair_cnt && g.cols_out % 512 == 0 && wide_units >= sms;
+    const bool pairs = g.flags & kFlagPairs;
+    bool wide = !pair_cnt && !pairs && g.cols_out % 512 == 0 && wide_units >= sms;
     if (tuning() & kTuneGemm2Narrow) wide = false;
-    if ((tuning() & kTuneGemm2Wide) && !pair_cnt && g.cols_out % 512 == 0) wide = true;
+    if ((tuning() & kTuneGemm2Wide) && !pair_cnt && !pairs && g.cols_out % 512 == 0) wide = true;
     Pair2Args P;
     std::memset(&P, 0, sizeof P);
     P.g = g;
@@ -488,7 +563,9 @@ void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
     P.no_wait = no_wait && !(tuning() & kTuneNoEarlyBackward) ? 1 : 0;
     P.release = release;
     P.own_cap = (tuning() & kTuneNoOwnBits) ? 0 : kMaxOwnUnits;
-    const int units = P.n_pair_rows * P.n_col_tiles;
+    // row-pair mode: the unit count is data-dependent (on the device); at most
+    // one unit per pair of mask columns per pair row
+    const int units = pairs ? P.n_pair_rows * (g.mask_cols / 2) : P.n_pair_rows * P.n_col_tiles;
     int clusters = std::min(units, sms / 2);
     if (clusters <= 0) return;
     cudaLaunchConfig_t cfg = {};

@@ -68,6 +68,9 @@ enum GemmFlags : uint32_t {
     kFlagReduce = 16u,  // split-K: split 0 stores, split j > 0 reduce-adds after split j - 1 (fixed order)
     kFlagOutMask = 32u,  // 2-CTA dense only: output blocks dropped in `words` (128x128, mask_cols
                          // per row) are written as +0.0 (dX at low p: masked dense, see sd_capi.cu)
+    kFlagPairs = 64u,    // dX split by mask-row pairs: the 2-CTA kernel computes the column blocks both
+                         // rows of a pair keep (taken in ascending pairs), the 1-CTA sdd kernel the
+                         // remainder and the zero fill (sd_gemm2.cu; mask_cols <= 64)
 };
 
 struct GemmArgs {
@@ -138,6 +141,8 @@ enum TuneFlags : int {
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
     kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
     kTuneNoMaskedDense = 1024,   // low-p dX stays on the sdd kernel instead of the masked 2-CTA dense GEMM
+    kTunePairs = 16384,          // mid-p plans split dX by mask-row pairs (2-CTA + 1-CTA remainder); off
+                                 // by default: bit-identical but not faster (profiles/r02_row_pairs_ab.txt)
     kTuneGemm2Narrow = 4096,     // 2-CTA kernel: always 256 x 256 pair tiles
     kTuneGemm2Wide = 8192,       // 2-CTA kernel: 256 x 512 pair tiles whenever the columns allow
     kTuneNoOwnBits = 2048,       // masked 2-CTA dX reads keep bits per chunk and releases at exit (the
@@ -163,6 +168,7 @@ inline void launch_gemm(const GemmCall& c, cudaStream_t s, bool no_wait = false)
 // pair tiles, static schedule. Used by launch_gemms when every problem of the
 // launch is dense and has at least one wave of pair tiles.
 bool gemm2_supported(const GemmArgs& a);
+bool gemm2_pairs_supported(const GemmArgs& a);
 void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tout, const GemmArgs& g,
                   const int32_t* pair_cnt, const int32_t* pair_idx, int pair_stride, cudaStream_t s,
                   bool no_wait = false, unsigned int* release = nullptr);

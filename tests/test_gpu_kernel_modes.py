@@ -386,3 +386,43 @@ def test_masked_dense_dx_wide_pairs_bitwise(sd, oracle, p):
         lib.sd_set_tuning(0)
     assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
     assert torch.equal(outs[1].view(torch.int16), outs[2].view(torch.int16))
+
+
+PAIR_CASES = [(4096, 4096, 4096, 0.5), (4096, 4096, 4096, 0.3), (2048, 2048, 8192, 0.7), (1024, 1536, 3072, 0.4),
+              (2048, 3072, 768, 0.5), (512, 640, 1152, 0.5)]
+
+
+@pytest.mark.parametrize("M,N,K,p", PAIR_CASES)
+@pytest.mark.parametrize("entry", ["fused", "dx_only"])
+def test_row_pair_dx_equals_sdd_bitwise(sd, oracle, M, N, K, p, entry):
+    """Mid-p dX split by mask-row pairs (kept blocks common to rows 2i and 2i+1,
+    in ascending pairs, on the 2-CTA kernel; the remainder + zero fill on the
+    1-CTA sdd kernel; tuning bit 16384) equals the plain sdd dX bit for bit,
+    dropped blocks exactly +0.0. Column counts C = K/128 of 32, 64, 24 (rows
+    straddling mask words), 6 and 9 (odd)."""
+    lib = sd.load_library()
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    outs = []
+    try:
+        for bits in (0, 16384):
+            lib.sd_set_tuning(bits)
+            plan = sd.LayerPlan(x, w, dy, p)
+            plan.forward(13)
+            plan.dx.fill_(float("nan"))
+            if entry == "fused":
+                plan.backward()
+            else:
+                plan.backward_dx()
+            torch.cuda.synchronize()
+            outs.append((plan.dx.clone(), plan.dw.clone() if entry == "fused" else None, plan.mask.words()))
+    finally:
+        lib.sd_set_tuning(0)
+    (dx0, dw0, m0), (dx1, dw1, m1) = outs
+    assert m0 == m1
+    assert torch.equal(dx0.view(torch.int16), dx1.view(torch.int16))
+    if dw0 is not None:
+        assert torch.equal(dw0, dw1)
+    R, C = M // 128, K // 128
+    bits = np.unpackbits(np.array(m0, dtype=np.uint64).view(np.uint8), bitorder="little")[: R * C].reshape(R, C)
+    blocks = dx0.view(R, 128, C, 128).permute(0, 2, 1, 3).reshape(R, C, -1)
+    assert (blocks[torch.from_numpy(bits == 0).cuda()].view(torch.int16) == 0).all()
