@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cmath>
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -494,5 +495,76 @@ inline LayerGrads backward(const LinearLayer& layer, const LayerContext& ctx, co
                                 m, n, k, stream));
     return g;
 }
+
+// ---------------------------------------------------------------- runtime objects
+
+// NCCL communicator owned by the library (sd_comm_*): rank 0 makes the id,
+// the caller broadcasts its 128 bytes (MPI, a file, a TCP store), every rank
+// constructs on its own device.
+class Communicator {
+public:
+    using Id = std::array<unsigned char, SD_COMM_ID_BYTES>;
+    static Id unique_id() {
+        Id id{};
+        check(sd_comm_unique_id(id.data()));
+        return id;
+    }
+    Communicator(int nranks, int rank, const Id& id) {
+        sd_comm* c = nullptr;
+        check(sd_comm_init(&c, nranks, rank, id.data()));
+        c_.reset(c);
+    }
+    void allreduce_sum(DeviceMatrix<float>& m, void* stream = nullptr) {
+        check(sd_comm_allreduce_sum(c_.get(), m.data(), m.size(), SD_DTYPE_F32, stream));
+    }
+    sd_comm* c() const { return c_.get(); }
+
+private:
+    struct Destroy {
+        void operator()(sd_comm* c) const { sd_comm_destroy(c); }
+    };
+    std::unique_ptr<sd_comm, Destroy> c_;
+};
+
+// A bound SparseDrop layer (sd_layer_plan): the forward/backward of
+// layer.hpp:85-162 on fixed device buffers, tensor maps encoded once — the
+// object a training loop keeps per layer. A row shard passes the global block
+// row of its first row (row_block_offset) so its mask rows equal the global
+// mask's; backward_allreduce then sums the shards' dW.
+class LayerPlan {
+public:
+    LayerPlan(const DeviceMatrix<bf16>& x, const DeviceMatrix<bf16>& w, const DeviceMatrix<bf16>& dy, double p,
+              int m_blk = 128, int k_blk = 128, int row_block_offset = 0, bool dy_ready = false)
+        : x_(x), w_(w), dy_(dy), y_(x.rows(), w.cols()), dx_(x.rows(), x.cols()), dw_(x.cols(), w.cols()),
+          mask_(x.rows() / m_blk, x.cols() / k_blk, m_blk, k_blk, row_block_offset) {
+        if (w.rows() != x.cols() || dy.rows() != x.rows() || dy.cols() != w.cols())
+            throw std::invalid_argument("layer shapes: x " + x.shape_string() + " w " + w.shape_string() + " dy " +
+                                        dy.shape_string());
+        sd_layer_plan* pl = nullptr;
+        check(sd_layer_plan_create(&pl, x.data(), w.data(), dy.data(), y_.data(), SD_DTYPE_BF16, dx_.data(),
+                                   SD_DTYPE_BF16, dw_.data(), SD_DTYPE_F32, x.rows(), w.cols(), x.cols(), p,
+                                   mask_.c()));
+        plan_.reset(pl);
+        if (dy_ready) check(sd_layer_plan_set_options(pl, SD_PLAN_DY_READY));
+    }
+    void forward(std::uint64_t seed, void* stream = nullptr) { check(sd_layer_plan_forward(plan_.get(), seed, stream)); }
+    void backward(void* stream = nullptr) { check(sd_layer_plan_backward(plan_.get(), stream)); }
+    void backward_allreduce(Communicator& comm, int nparts = 2, void* stream = nullptr, void* comm_stream = nullptr) {
+        check(sd_layer_plan_backward_allreduce(plan_.get(), comm.c(), nparts, stream, comm_stream));
+    }
+    const DeviceMatrix<bf16>& y() const { return y_; }
+    const DeviceMatrix<bf16>& dx() const { return dx_; }
+    DeviceMatrix<float>& dw() { return dw_; }
+    const BlockMask& mask() const { return mask_; }
+
+private:
+    struct Destroy {
+        void operator()(sd_layer_plan* p) const { sd_layer_plan_destroy(p); }
+    };
+    DeviceMatrix<bf16> x_, w_, dy_, y_, dx_;
+    DeviceMatrix<float> dw_;
+    BlockMask mask_;
+    std::unique_ptr<sd_layer_plan, Destroy> plan_;
+};
 
 }  // namespace sparsedrop::b200

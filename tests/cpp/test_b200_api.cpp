@@ -303,3 +303,45 @@ TEST_CASE("layer forward/backward (sparsedrop) match the oracle") {
     CHECK(rel_frob(g.dw.to_host(), dw) < 1e-5);
     CHECK_THROWS_AS(backward(layer, ctx, x), std::invalid_argument);
 }
+
+// SURVEY §8e through the C++ API: two row shards of one layer, each with its own
+// plan (row_block_offset = its first global block row) — their masks are the
+// global mask's rows, and the sum of their dW (what the NCCL all-reduce forms on
+// G GPUs) equals the unsharded dW within fp32 reassociation. backward_allreduce
+// runs on a 1-rank communicator (one GPU here): the identity, so it must equal
+// the plain backward bit for bit.
+TEST_CASE("row-sharded layer plans and the dW all-reduce") {
+    const int M = 512, N = 256, K = 384;
+    const double p = 0.4;
+    const auto xh = random_matrix(M, K, 11), wh = random_matrix(K, N, 12), dyh = random_matrix(M, N, 13);
+    auto x = DeviceMatrix<bf16>::from_host(M, K, xh), w = DeviceMatrix<bf16>::from_host(K, N, wh);
+    auto dy = DeviceMatrix<bf16>::from_host(M, N, dyh);
+    LayerPlan full(x, w, dy, p);
+    full.forward(77);
+    full.backward();
+    const auto dw_full = full.dw().to_host();
+    const auto words_full = full.mask().words();
+    std::vector<double> dw_sum(static_cast<std::size_t>(K) * N, 0.0);
+    Communicator comm(1, 0, Communicator::unique_id());
+    for (int shard = 0; shard < 2; ++shard) {
+        const int r0 = shard * M / 2;
+        std::vector<float> xs(xh.begin() + static_cast<std::ptrdiff_t>(r0) * K,
+                              xh.begin() + static_cast<std::ptrdiff_t>(r0 + M / 2) * K);
+        std::vector<float> dys(dyh.begin() + static_cast<std::ptrdiff_t>(r0) * N,
+                               dyh.begin() + static_cast<std::ptrdiff_t>(r0 + M / 2) * N);
+        auto xg = DeviceMatrix<bf16>::from_host(M / 2, K, xs), dyg = DeviceMatrix<bf16>::from_host(M / 2, N, dys);
+        LayerPlan part(xg, w, dyg, p, 128, 128, r0 / 128);
+        part.forward(77);
+        part.backward();
+        const auto dw_plain = part.dw().to_host();
+        const auto ws = part.mask().words();
+        for (int r = 0; r < M / 256; ++r)
+            for (int c = 0; c < K / 128; ++c)
+                CHECK(kept_host(ws, K / 128, r, c) == kept_host(words_full, K / 128, r0 / 128 + r, c));
+        part.forward(77);
+        part.backward_allreduce(comm, 3);
+        CHECK(part.dw().to_host() == dw_plain);  // 1-rank all-reduce: identity, slabs bit-identical
+        for (std::size_t i = 0; i < dw_sum.size(); ++i) dw_sum[i] += dw_plain[i];
+    }
+    CHECK(rel_frob(dw_full, dw_sum) < 1e-6);
+}
