@@ -264,19 +264,35 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
             for (int i = __popcll(common) & ~1; i < __popcll(common); ++i) paired &= ~(1ull << (63 - __clzll(paired)));
             uint64_t rem = mine & ~paired;
             for (int i = 0; i < cu * per_unit && rem; ++i) rem &= rem - 1;  // skip earlier units' blocks
-            for (int j = 0; j < per_unit; ++j) {
+            // slots and zero blocks fill in prefix order: constant indices after
+            // unrolling keep the Unit in registers (no local-memory stack frame)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j >= per_unit) break;
                 const int li = cu * per_unit + j;
                 if (rem) {
-                    t.slot_blk[t.nslots++] = __ffsll(static_cast<long long>(rem)) - 1;
+                    t.slot_blk[j] = __ffsll(static_cast<long long>(rem)) - 1;
+                    t.nslots = j + 1;
                     rem &= rem - 1;
                 }
-                if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
+                if (li < ndrop) {
+                    t.zero_blk[j] = __ldcg(row + a.mask_cols - 1 - li);
+                    t.nzero = j + 1;
+                }
             }
         } else {
-            for (int j = 0; j < per_unit; ++j) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j >= per_unit) break;
                 const int li = cu * per_unit + j;
-                if (li < cnt) t.slot_blk[t.nslots++] = __ldcg(row + li);
-                if (li < ndrop) t.zero_blk[t.nzero++] = __ldcg(row + a.mask_cols - 1 - li);
+                if (li < cnt) {
+                    t.slot_blk[j] = __ldcg(row + li);
+                    t.nslots = j + 1;
+                }
+                if (li < ndrop) {
+                    t.zero_blk[j] = __ldcg(row + a.mask_cols - 1 - li);
+                    t.nzero = j + 1;
+                }
             }
         }
         t.n_eff = t.nslots * a.out_col_blk;
@@ -355,8 +371,9 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
         }
     };
     if (sdd) {
-        for (int z = 0; z < t.nzero; ++z)
-            zero_rows<OUT_F32>(a, row_first, t.zero_blk[z] * a.out_col_blk, a.out_col_blk, lane);
+#pragma unroll
+        for (int z = 0; z < 4; ++z)
+            if (z < t.nzero) zero_rows<OUT_F32>(a, row_first, t.zero_blk[z] * a.out_col_blk, a.out_col_blk, lane);
     }
     if (t.n_eff == 0) {
         const int rem = a.cols_out - t.n0;
@@ -445,7 +462,8 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
             if (sdd) {
                 const int tcol = c * kChunkCols;
                 const int sl = tcol / a.out_col_blk;
-                col = t.slot_blk[sl] * a.out_col_blk + (tcol - sl * a.out_col_blk);
+                const int blk = sl == 0 ? t.slot_blk[0] : sl == 1 ? t.slot_blk[1] : sl == 2 ? t.slot_blk[2] : t.slot_blk[3];
+                col = blk * a.out_col_blk + (tcol - sl * a.out_col_blk);
             } else {
                 col = t.n0 + c * kChunkCols;
             }
@@ -522,7 +540,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // through a possibly stale L1 line of an earlier grid.
     if (!L.no_wait) ptx::pdl_wait();
     ptx::pdl_launch_dependents();
+#ifdef SD_TRACE
     long long tr[16] = {0};
+#else
+    long long* tr = nullptr;  // per-role wait counters exist only in SD_TRACE builds
+#endif
 #ifdef SD_TRACE
     const long long t_start = clock64();
     const unsigned long long g_start = gtimer();
@@ -630,6 +652,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         } else {
                             const int per = a.out_col_blk / 128;
+                            // (a runtime slot index reads cur from local memory; unrolling it
+                            // with constant indices instead bloated this single-thread loop
+                            // and made sdd 4-7% slower: profiles/r02_local_memory_ab.txt)
                             const int sl_end = min(cur.nslots, (h + 1) * per_half);
                             for (int sl = h * per_half; sl < sl_end; ++sl) {
                                 const int col0 = cur.slot_blk[sl] * a.out_col_blk;
