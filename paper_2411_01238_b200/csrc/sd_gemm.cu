@@ -597,6 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int per_half = sdd ? kBN / a.out_col_blk : 0;    // sdd blocks per B slot
                 const int spb = a.red_blk / kBK;
                 const int li0 = sdd ? 0 : cur.first_entry;
+                const int scol0 = cur.slot_blk[0] * a.out_col_blk, scol1 = cur.slot_blk[1] * a.out_col_blk;
+                const int scol2 = cur.slot_blk[2] * a.out_col_blk, scol3 = cur.slot_blk[3] * a.out_col_blk;
                 const int32_t* lst =
                     (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
                                          : nullptr;
@@ -652,12 +654,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         } else {
                             const int per = a.out_col_blk / 128;
-                            // (a runtime slot index reads cur from local memory; unrolling it
-                            // with constant indices instead bloated this single-thread loop
-                            // and made sdd 4-7% slower: profiles/r02_local_memory_ab.txt)
+                            // slot columns by select from per-unit scalars: a runtime index
+                            // into cur puts the Unit in local memory, and unrolling with
+                            // constant indices bloated this single-thread loop (sdd 4-7%
+                            // slower: profiles/r02_local_memory_ab.txt)
                             const int sl_end = min(cur.nslots, (h + 1) * per_half);
                             for (int sl = h * per_half; sl < sl_end; ++sl) {
-                                const int col0 = cur.slot_blk[sl] * a.out_col_blk;
+                                const int col0 = (sl == 0 ? scol0 : sl == 1 ? scol1 : sl == 2 ? scol2 : scol3);
                                 const int off = (sl - h * per_half) * per;
                                 for (int j = 0; j < per; ++j) {
                                     if (!b_mn)
