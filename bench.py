@@ -147,28 +147,47 @@ def cpu_baseline(size, p, budget_s=12.0):
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU layer fwd+bwd (oracle/_ref, else the oracle port)
+    on the box's host cores, on the GPU arm's config/metric: a bounded slab of
+    the same problem per step (work is linear in the slab), rank 0 only."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     kind, run = _cpu_layer_runner()
-    n_slab = max(128, min(args.size, 512))
-    x, w, dy = cpu_sample_inputs(args.size, n_slab)
+    if args.config == "cfg5":
+        # a 2048-row slab of M (16 tile rows: the reference parallelises over them)
+        from oracle.oracle import Oracle
+
+        o = Oracle()
+        bf = lambda r, c, sd_: o.bf16_bits_to_f64(o.to_bf16_bits(o.random_matrix(r, c, sd_))).astype("float32")  # noqa: E731
+        rows = min(2048, args.m_global)
+        x, w, dy = bf(rows, args.kn, 1), bf(args.kn, args.kn, 2), bf(rows, args.kn, 3)
+        flops = 3 * 2 * rows * args.kn * args.kn
+        config = cfg5_config(args.m_global, args.kn, args.p, world, max(1, args.dw_parts), args.dist_backend)
+        scaling = "strong"
+        sample = (f"per step: the reference layer fwd+bwd on a {rows}-row slab of M (K=N={args.kn}; every GEMM of "
+                  f"the layer is linear in M), {threads} host threads; value = slab FLOPs / slab time")
+    else:
+        n_slab = max(128, min(args.size, 512))
+        x, w, dy = cpu_sample_inputs(args.size, n_slab)
+        flops = 3 * 2 * args.size * n_slab * args.size
+        config = workload_config(args.size, args.p, world, args.dw_parts)
+        scaling = "weak"
+        sample = (f"per step: the reference layer fwd+bwd at M=K={args.size}, N-column slab {n_slab} (work linear "
+                  f"in N), {threads} host threads")
     for _ in range(args.warmup):
         run(x, w, dy, args.p, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         run(x, w, dy, args.p, threads)
     dt = (time.perf_counter() - t0) / args.steps
-    flops = 3 * 2 * args.size * n_slab * args.size
     value = flops / dt / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference random_matrix)",
-        "config": workload_config(args.size, args.p, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"per step: the reference layer fwd+bwd at M=K={args.size}, N-column slab "
-                                   f"{n_slab} (work linear in N), {threads} host threads"},
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference random_matrix)",
+        "config": config,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
