@@ -494,9 +494,17 @@ def main():
     lib = sd.load_library()
     import ctypes as _ct
 
-    def rot_ms(fns, steps):
-        for j in range(3 * n_sets):
+    def rot_ms(fns, steps, settle_s=1.0):
+        # each kernel in its own settled power-capped state, like every other leg
+        # (without it the kernel times depended on which leg ran before: a fused
+        # backward read 133 us in one run and 156 us in the next)
+        t_end = time.perf_counter() + (settle_s if args.preroll > 0 else 0.0)
+        j = 0
+        while j < 3 * n_sets or time.perf_counter() < t_end:
             fns[j % n_sets]()
+            j += 1
+            if j % 64 == 0:
+                torch.cuda.synchronize()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -558,8 +566,8 @@ def main():
         "peak_sustained": float(peaks.get("bf16_tflops_sustained", 1400.0)),
         "frac_of_sustained": achieved / float(peaks.get("bf16_tflops_sustained", 1400.0)),
         "kernel_ms": kms,
-        "kernel_timing": "each kernel back-to-back over the rotating input sets (mask_gen is host-launch-bound "
-                         "here; ncu: ~5-7 us)",
+        "kernel_timing": "each kernel back-to-back over the rotating input sets after 1 s of its own sustained "
+                         "load (mask_gen is host-launch-bound here; ncu: ~5-7 us)",
     }
 
     # ---- sweep
