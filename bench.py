@@ -478,15 +478,15 @@ def main():
         finally:
             _lib_t.sd_set_tuning(0)
 
-    # our dense step and cuBLAS alternate over two rounds, each leg after its own
-    # settle; the better round of each is kept (a single cuBLAS leg once read 15%
-    # faster than in the next run while both rounds of tools/ab_settled.py put it
-    # within 1% of our step at 4096^3: profiles/r02_dense_vs_cublas_ab.txt)
+    # our dense step and cuBLAS alternate over three rounds, each leg after its
+    # own settle; the median round of each is reported. Under the power cap a
+    # cuBLAS leg is bimodal (0.276 or 0.323 ms at 4096^3 in consecutive rounds of
+    # one run; ours 0.313-0.320): profiles/r02_dense_vs_cublas_ab.txt
     rounds = {"dense": [], "torch": []}
-    for _ in range(2):
+    for _ in range(3):
         rounds["dense"].append(time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle))
         rounds["torch"].append(time_steps(torch_step, args.steps, args.warmup, preroll_s=settle))
-    ms_dense, ms_torch = min(rounds["dense"]), min(rounds["torch"])
+    ms_dense, ms_torch = sorted(rounds["dense"])[1], sorted(rounds["torch"])[1]
     ms_dense_1cta = dense_1cta_step()
 
     # ---- per-kernel durations at the headline p (roofline): each kernel run
