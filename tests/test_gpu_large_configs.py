@@ -259,3 +259,67 @@ def test_split_k_dw_deterministic(sd):
         else:
             assert torch.equal(plan.dw, ref)
     assert not torch.isnan(ref).any()
+
+
+@pytest.mark.parametrize("p", [0.1, 0.5])
+def test_cfg3_vit_mlp_full_size(sd, oracle, p):
+    """configs[2] at full size: the ViT-B MLP training step, 65536 tokens,
+    768 -> 3072 -> 768, SparseDrop before each Linear (GELU between). Every GEMM
+    of the step against the oracle on sampled slabs of its own inputs (the
+    step's bf16 intermediates), masks bit-exact from effective_seed(seed, step,
+    layer) (layer.hpp:64-67); GELU' consumed exactly as computed."""
+    from paper_2411_01238_b200.mlp import SparseDropMLP, gelu_grad
+
+    M, D, H = 65536, 768, 3072
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(91 + int(10 * p))
+    x, w1, w2, dy = _rand(gen, M, D), _rand(gen, D, H), _rand(gen, H, D), _rand(gen, M, D)
+    mlp = SparseDropMLP(x, w1, w2, dy, p, seed=17)
+    mlp.step(step_seed=4)
+    torch.cuda.synchronize()
+    s = sd.dropout_scale(p)
+    f1, f2 = mlp.fc1, mlp.fc2
+    b1 = _mask_bits(oracle, f1, p, oracle.effective_seed(17, 4, 0))
+    b2 = _mask_bits(oracle, f2, p, oracle.effective_seed(17, 4, 1))
+    assert torch.equal(mlp.act, __import__("paper_2411_01238_b200.mlp", fromlist=["gelu"]).gelu(f1.y))
+    assert torch.equal(mlp.dact, gelu_grad(f1.y, f2.dx))
+    # fc2: y = s (act . m1) W2, dW2 over all 65536 rows (split-K at p=0.1), dX2 (= d act)
+    _check_rows(oracle, f2, b2, s, rows=[0, 300, 511], nslab=(0, 768), kslab=(2560, 3072))
+    _check_dw(oracle, f2, b2, s, kbs=[0, 23], nslabs=[(256, 512)])
+    # fc1: h = s (x . m0) W1, dW1 from dact over all rows, dX1
+    _check_rows(oracle, f1, b1, s, rows=[7, 450], nslab=(1024, 1536), kslab=(0, 768))
+    _check_dw(oracle, f1, b1, s, kbs=[0, 5], nslabs=[(0, 256), (2816, 3072)])
+
+
+def test_cfg5_eight_uneven_row_shards(sd):
+    """configs[4]'s decomposition over G = 8 ranks at reduced size, with uneven
+    shards (60 block rows over 8 ranks: paper_2411_01238_b200.sharding): each
+    shard's mask equals the global mask's rows, Y and dX rows are bit-identical
+    to the unsharded layer's, and the 8 partial dWs sum to the full dW (the
+    all-reduce's result) within fp32 reassociation."""
+    from paper_2411_01238_b200.sharding import all_shards
+
+    M, N, K, p, G = 128 * 60, 1024, 2048, 0.5, 8
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(101)
+    x, w, dy = _rand(gen, M, K), _rand(gen, K, N), _rand(gen, M, N)
+    full = sd.LayerPlan(x, w, dy, p)
+    full.forward(seed=23)
+    full.backward()
+    words_full = np.array(full.mask.words(), dtype=np.uint64)
+    bits_full = _bits(words_full, M // 128, K // 128)
+    acc = torch.zeros(K, N, dtype=torch.float64, device="cuda")
+    shards = all_shards(M, 128, G)
+    assert sorted({sh.rows // 128 for sh in shards}) == [7, 8]
+    for sh in shards:
+        r0, r1 = sh.row0, sh.row0 + sh.rows
+        pl = sd.LayerPlan(x[r0:r1].contiguous(), w, dy[r0:r1].contiguous(), p, row_block_offset=sh.row_block_offset)
+        pl.forward(seed=23)
+        pl.backward()
+        torch.cuda.synchronize()
+        b = _bits(np.array(pl.mask.words(), dtype=np.uint64), sh.rows // 128, K // 128)
+        assert np.array_equal(b, bits_full[r0 // 128:r1 // 128])
+        assert torch.equal(pl.y, full.y[r0:r1]) and torch.equal(pl.dx, full.dx[r0:r1])
+        acc += pl.dw.double()
+    relf = ((acc - full.dw.double()).norm() / full.dw.double().norm()).item()
+    assert relf < 1e-6, relf
