@@ -1048,6 +1048,9 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         if (!comm) fail(SD_EINVAL, "sd_layer_plan_backward_allreduce: null communicator");
+        if (comm_device(comm) != plan->device)
+            fail(SD_EINVAL, "sd_layer_plan_backward_allreduce: communicator on device " + str(comm_device(comm)) +
+                                ", plan on device " + str(plan->device));
         const int cblocks = plan->mask.block_cols;
         if (nparts < 1 || nparts > cblocks)
             fail(SD_ERANGE, "backward_allreduce: nparts " + str(nparts) + " out of range for " + str(cblocks) +
@@ -1062,7 +1065,6 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
         }
         if (!plan->reduced) check_cuda(cudaEventCreateWithFlags(&plan->reduced, cudaEventDisableTiming), "cudaEventCreate");
         const bool f32 = plan->dw.args.flags & kFlagF32;
-        const size_t el = f32 ? 4 : 2;
         const bool nw = take_no_wait(plan, s);
         // dW slab by slab (mask-column blocks, the same tiles and reduction
         // order as the full dW): slab i's all-reduce runs on the comm stream
@@ -1076,7 +1078,6 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
             }
             comm_allreduce_sum(comm, g.args.out, static_cast<size_t>(g.args.rows_out) * g.args.cols_out,
                                f32 ? SD_DTYPE_F32 : SD_DTYPE_BF16, cs);
-            (void)el;
         }
         if (use_pairs(plan)) {
             launch_dx_pairs(plan, s, false);

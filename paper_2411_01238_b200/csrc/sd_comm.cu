@@ -130,6 +130,7 @@ void comm_allreduce_sum(sd_comm* c, void* buf, size_t count, int dtype, cudaStre
 }
 
 int comm_nranks(const sd_comm* c) { return c->nranks; }
+int comm_device(const sd_comm* c) { return c->device; }
 
 }  // namespace sd
 

@@ -186,5 +186,6 @@ CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint
 // In-place sum all-reduce of `count` elements (SD_DTYPE_*) on stream s.
 void comm_allreduce_sum(sd_comm* c, void* buf, size_t count, int dtype, cudaStream_t s);
 int comm_nranks(const sd_comm* c);
+int comm_device(const sd_comm* c);
 
 }  // namespace sd
