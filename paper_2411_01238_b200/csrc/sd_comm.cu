@@ -174,8 +174,9 @@ int sd_comm_init(sd_comm** out, int32_t nranks, int32_t rank, const void* id) {
 int sd_comm_destroy(sd_comm* c) {
     return guarded_comm([&] {
         if (!c) return;
-        if (c->comm) check_nccl(nccl().comm_destroy(c->comm), "ncclCommDestroy");
-        delete c;
+        const ncclResult_t r = c->comm ? nccl().comm_destroy(c->comm) : ncclSuccess;
+        delete c;  // freed either way; a failed destroy is still reported
+        check_nccl(r, "ncclCommDestroy");
     });
 }
 
