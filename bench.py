@@ -851,6 +851,20 @@ def run_cfg5(args, rank, world, dev_index, dev):
         "note": "device-timed, max over ranks: allreduce_ms = the dW all-reduce alone; compute_only = the "
                 "same step without it; overlap_fraction = 1 - (step - compute_only) / allreduce",
     }
+    # roofline of the per-GPU step's GEMM work (the step's kernels overlap under
+    # PDL, so the whole compute-only step is the timed unit here)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    achieved = keep * 3 * 2 * M * KN * KN / (ms_compute * 1e-3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "the per-GPU step without the all-reduce (mask + forward + backward GEMMs)",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (steps timed after a sustained pre-roll)",
+            "algorithmic_per_launch": {"flops": keep * 3 * 2 * M * KN * KN,
+                                       "note": "executed: keep x 3 GEMMs x 2 M_local N K per step"}}
     # e2e through the public API with host buffers (pinned), every step
     e2e = None
     if not args.no_e2e:
@@ -892,6 +906,7 @@ def run_cfg5(args, rank, world, dev_index, dev):
             "config": cfg5_config(MG, KN, p, world, nparts, args.dist_backend),
             "keep_fraction": keep, "executed_tflops": value * keep,
             "comm": comm_info, "gpu_launches": launches,
+            "roofline": roof,
             "gpu_launches_note": "per step: mask, forward, " + (f"{nparts} dW slabs, dX" if world > 1 else
                                                                "fused dW+dX (or dW + masked dX at low p)"),
             "cpu_baseline": None,
