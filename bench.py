@@ -326,7 +326,7 @@ def main():
     def flush():
         flush_buf.fill_(float(len(str(flush_buf.numel()))))
 
-    def time_steps(step, steps, warmup, preroll_s=None, rotate=None):
+    def time_steps(step, steps, warmup, preroll_s=None, rotate=None, windows=1):
         preroll_s = args.preroll if preroll_s is None else preroll_s
         rotate = (n_sets > 1) if rotate is None else rotate
         """Device time per step (CUDA events on the launching stream, max over
@@ -334,7 +334,10 @@ def main():
         input sets whose combined footprint exceeds L2; else: L2 flushed before
         every step outside the per-step events. A short sustained pre-roll of
         the same step first, so every configuration is timed in the same
-        (power-capped) steady state rather than a cold burst."""
+        (power-capped) steady state rather than a cold burst. windows > 1
+        (legs other than the headline): that many consecutive windows of
+        `steps` steps, the median window is returned (one host hiccup while
+        enqueueing once doubled a sweep point)."""
         if preroll_s > 0:
             # estimate the step time, then run the same number of pre-roll steps
             # on every rank (each step may contain a collective)
@@ -359,14 +362,23 @@ def main():
         l0 = sd.launch_count()
         if rotate:
             # back-to-back steps over rotating input sets (combined > L2): one
-            # event pair around exactly `steps` steps
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for i in range(steps):
-                step(warmup + i)
-            b.record()
+            # event pair around exactly `steps` steps. One untimed step is
+            # enqueued first, so the GPU is busy (and the host ahead of it) when
+            # the start event is reached: no launch-latency gap inside the window
+            step(warmup + steps)
+            l0 = sd.launch_count()
+            evs = []
+            for wi in range(windows):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for i in range(steps):
+                    step(warmup + i)
+                b.record()
+                evs.append((a, b))
             torch.cuda.synchronize()
-            total_ms = a.elapsed_time(b)
+            win = sorted(a_.elapsed_time(b_) for a_, b_ in evs)
+            total_ms = win[len(win) // 2]
+            launches = (sd.launch_count() - l0) // windows
         else:
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(steps)]
@@ -377,9 +389,10 @@ def main():
                 evs[i][1].record()
             torch.cuda.synchronize()
             total_ms = sum(a_.elapsed_time(b_) for a_, b_ in evs)
+            launches = sd.launch_count() - l0
         barrier()
         torch.cuda.synchronize()
-        launch_box[0] = sd.launch_count() - l0
+        launch_box[0] = launches
         return max_over_ranks(total_ms) / steps
 
     plans = {}
@@ -474,7 +487,7 @@ def main():
         # (tuning 16: no 2-CTA kernel) — the like-for-like (1-p) reference
         _lib_t.sd_set_tuning(16)
         try:
-            return time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle)
+            return time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle, windows=3)
         finally:
             _lib_t.sd_set_tuning(0)
 
@@ -484,8 +497,8 @@ def main():
     # one run; ours 0.313-0.320): profiles/r02_dense_vs_cublas_ab.txt
     rounds = {"dense": [], "torch": []}
     for _ in range(3):
-        rounds["dense"].append(time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle))
-        rounds["torch"].append(time_steps(torch_step, args.steps, args.warmup, preroll_s=settle))
+        rounds["dense"].append(time_steps(dense_step_fn(), args.steps, args.warmup, preroll_s=settle, windows=3))
+        rounds["torch"].append(time_steps(torch_step, args.steps, args.warmup, preroll_s=settle, windows=3))
     ms_dense, ms_torch = sorted(rounds["dense"])[1], sorted(rounds["torch"])[1]
     ms_dense_1cta = dense_1cta_step()
 
@@ -579,7 +592,7 @@ def main():
     sweep = []
     if not args.no_sweep:
         for p in SWEEP_P:
-            msp = time_steps(sparse_step_fn(p), max(5, args.steps // 2), 3, preroll_s=settle)
+            msp = time_steps(sparse_step_fn(p), max(5, args.steps // 2), 3, preroll_s=settle, windows=3)
             pl = plan_for(p)
             kp = pl.mask.keep_count() / pl.mask.total_blocks()
             sweep.append({
@@ -607,7 +620,7 @@ def main():
                 pl8.forward(seed=sd.effective_seed(0, i, 0))
                 pl8.backward()
 
-            ms8 = time_steps(st8, max(5, args.steps // 2), 3, preroll_s=settle)
+            ms8 = time_steps(st8, max(5, args.steps // 2), 3, preroll_s=settle, windows=3)
             k8 = pl8.mask.keep_count() / pl8.mask.total_blocks()
             ex8 = k8 * 3 * 2 * S8 ** 3 / (ms8 * 1e-3) / 1e12
             t8[f"p{p8}"] = {"ms_per_step": ms8, "keep": k8,
@@ -620,13 +633,13 @@ def main():
                     pl8.dense_forward()
                     pl8.dense_backward()
 
-                msd8 = time_steps(dn8, max(5, args.steps // 2), 3, preroll_s=settle)
+                msd8 = time_steps(dn8, max(5, args.steps // 2), 3, preroll_s=settle, windows=3)
                 t8["dense_ms_per_step"] = msd8
                 t8["dense_tflops"] = 3 * 2 * S8 ** 3 / (msd8 * 1e-3) / 1e12
                 t8["speedup_vs_dense_p0.5"] = msd8 / ms8
             del pl8
         mst = time_steps(lambda i: (x8 @ w8, x8.t() @ dy8, dy8 @ w8.t()), max(5, args.steps // 2), 3,
-                         preroll_s=settle)
+                         preroll_s=settle, windows=3)
         t8["torch_cublas_dense_tflops"] = 3 * 2 * S8 ** 3 / (mst * 1e-3) / 1e12
         del x8, w8, dy8
         torch.cuda.empty_cache()
@@ -665,6 +678,20 @@ def main():
                "pcie_gbps": (pipe.h2d_bytes + pipe.d2h_bytes) / (ms_e2e * 1e-3) / 1e9}
         del pipe
 
+    # configs[4] on this one GPU (the G = 1 point of its strong-scaling curve: the
+    # N > 1 runs of this script measure configs[4] by default)
+    cfg5_g1 = None
+    if world == 1 and not args.no_sweep:
+        import copy
+
+        a5 = copy.copy(args)
+        a5.steps, a5.warmup, a5.no_e2e, a5.config = max(5, args.steps // 2), 3, True, "cfg5"
+        l5 = run_cfg5(a5, rank, world, dev_index, dev, emit=False)
+        cfg5_g1 = {k: l5[k] for k in ("value", "unit", "ms_per_step", "executed_tflops", "keep_fraction", "config",
+                                      "roofline", "clocks", "gpu_launches")}
+        cfg5_g1["note"] = ("configs[4] (M=524288, K=N=8192, p=%g) on one B200: the strong-scaling baseline for the "
+                           "N > 1 runs (torchrun ... bench.py --gpus N, default --config cfg5)" % args.p)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -686,16 +713,18 @@ def main():
                            "dense_1cta_ms_per_step: the same dense step on the 1-CTA tiles the masked GEMMs use"),
             "isolated_ms_per_step": ms_isolated,
             "timing": (f"{n_sets} rotating input sets ({n_sets * set_bytes / 2**20:.0f} MiB > L2), steps back-to-back, "
-                       "one CUDA-event pair around the K timed steps; every leg (headline, dense, sweep points, t8) "
-                       "after 1.5 s of its own sustained load (power-capped steady state); isolated_ms_per_step: "
-                       "one step at a time with a 512 MiB L2 flush before each, per-step events (includes launch "
-                       "latency)"),
+                       "one CUDA-event pair around the K timed steps, entered with one untimed step already queued "
+                       "(no launch-latency gap in the window); every leg (headline, dense, sweep points, t8) after "
+                       "1.5 s of its own sustained load (power-capped steady state); legs other than the headline: "
+                       "median of three consecutive K-step windows; isolated_ms_per_step: one step at a time with a "
+                       "512 MiB L2 flush before each, per-step events (includes launch latency)"),
             "torch_cublas_dense_ms_per_step": ms_torch,
             "dense_rounds_ms": rounds["dense"], "torch_cublas_rounds_ms": rounds["torch"],
             "gpu_launches": gpu_launches,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "sweep": sweep,
             "t8": t8,
+            "cfg5_g1": cfg5_g1,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -722,9 +751,10 @@ def cfg5_config(m_global, kn, p, world, nparts, backend):
     }
 
 
-def run_cfg5(args, rank, world, dev_index, dev):
+def run_cfg5(args, rank, world, dev_index, dev, emit=True):
     """configs[4]: M=524288, K=N=8192 strong-scaled over the ranks.
-    value = 3*2*M*N*K (dense-equivalent, whole job) / max-over-ranks step time."""
+    value = 3*2*M*N*K (dense-equivalent, whole job) / max-over-ranks step time.
+    Returns the line (rank 0); prints it when `emit`."""
     import torch
     import torch.distributed as dist
 
@@ -913,10 +943,14 @@ def run_cfg5(args, rank, world, dev_index, dev):
             "cpu_baseline_note": "the reference CPU path is timed in the configs[1] line (N=1 default run)",
             "e2e": e2e, "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
     if comm is not None:
         torch.cuda.synchronize()
         comm.close()
+    del x, w, dy
+    torch.cuda.empty_cache()
+    return line if rank == 0 else None
 
 
 if __name__ == "__main__":
