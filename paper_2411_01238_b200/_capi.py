@@ -82,6 +82,7 @@ PROTOTYPES = {
     "sd_layer_plan_dense_forward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_dense_backward": (ctypes.c_int, [_P, _P]),
     "sd_layer_plan_set_options": (ctypes.c_int, [_P, _I]),
+    "sd_layer_plan_graph_step": (ctypes.c_int, [_P, ctypes.c_uint64, _I, _P]),
     "sd_layer_plan_destroy": (ctypes.c_int, [_P]),
     "sd_comm_unique_id": (ctypes.c_int, [_P]),
     "sd_comm_init": (ctypes.c_int, [ctypes.POINTER(_P), _I, _I, _P]),

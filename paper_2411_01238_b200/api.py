@@ -488,6 +488,13 @@ class LayerPlan:
         check(_lib().sd_layer_plan_backward(self._plan, ctypes.c_void_p(_stream(stream))))
         return self.dx, self.dw
 
+    def graph_step(self, seed: int, backward: bool = True, stream=None):
+        """forward(seed) [+ backward()] as ONE CUDA-graph launch
+        (sd_layer_plan_graph_step): for host-bound callers; same results."""
+        check(_lib().sd_layer_plan_graph_step(self._plan, seed & MASK64, 3 if backward else 1,
+                                               ctypes.c_void_p(_stream(stream))))
+        return self.y
+
     def backward_dw(self, stream=None):
         check(_lib().sd_layer_plan_backward_dw(self._plan, ctypes.c_void_p(_stream(stream))))
         return self.dw

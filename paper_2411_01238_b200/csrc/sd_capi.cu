@@ -732,9 +732,26 @@ struct sd_layer_plan {
     // dW slab (compute -> comm stream) and one for the last all-reduce
     std::vector<cudaEvent_t> slab_done;
     cudaEvent_t reduced = nullptr;
+    // CUDA-graph replays of the step (sd_layer_plan_graph_step): [0] forward,
+    // [1] forward + backward; captured once on a private stream, the mask
+    // kernel node's seed patched per replay
+    struct GraphStep {
+        cudaGraph_t graph = nullptr;  // kept: its mask node is the handle the exec update needs
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t mask_node = nullptr;
+        cudaKernelNodeParams mask_params{};
+        std::vector<unsigned char> mask_args;
+        uint64_t kernels = 0;
+    } graph[2];
+    cudaStream_t capture_stream = nullptr;
     ~sd_layer_plan() {
         for (cudaEvent_t e : slab_done) cudaEventDestroy(e);
         if (reduced) cudaEventDestroy(reduced);
+        for (auto& g : graph) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
+        if (capture_stream) cudaStreamDestroy(capture_stream);
     }
 };
 
@@ -1014,13 +1031,17 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
 // (all-kept) mask is still generated: the caller's BlockMask stays valid.
 static bool plan_dense(const sd_layer_plan* plan) { return plan->p == 0.0 && !(tuning() & kTuneNarrow); }
 
+static void plan_forward_impl(sd_layer_plan* plan, uint64_t seed, cudaStream_t s) {
+    launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, s);
+    launch_gemm(plan_dense(plan) ? plan->dense_fwd : plan->fwd, s);
+    plan->fwd_mark = sd_launch_count();
+    plan->fwd_stream = s;
+}
+
 int sd_layer_plan_forward(sd_layer_plan* plan, uint64_t seed, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, as_stream(stream));
-        launch_gemm(plan_dense(plan) ? plan->dense_fwd : plan->fwd, as_stream(stream));
-        plan->fwd_mark = sd_launch_count();
-        plan->fwd_stream = as_stream(stream);
+        plan_forward_impl(plan, seed, as_stream(stream));
     });
 }
 
@@ -1105,25 +1126,104 @@ int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     });
 }
 
+static void plan_backward_impl(sd_layer_plan* plan, cudaStream_t s) {
+    const bool nw = take_no_wait(plan, s);
+    if (plan_dense(plan)) {
+        fused_backward(plan->dense_dx, plan->dense_dw, s, nw);
+    } else if (use_masked_dx(plan)) {
+        // dW on the 1-CTA kernel, dX on the 2-CTA kernel: independent
+        // launches, the second never waits for the first
+        launch_gemm(plan->dw, s, nw);
+        launch_gemm(plan->dx_masked, s, true);
+    } else if (use_pairs(plan)) {
+        // dX's row-pair part on the 2-CTA kernel, then dX's remainder and dW
+        // as one 1-CTA launch that fills the SMs the first one leaves
+        launch_dx_pairs(plan, s, nw);
+        fused_backward(plan->dx_rem, plan->dw, s, true);
+    } else {
+        fused_backward(plan->dx, plan->dw, s, nw);
+    }
+}
+
 int sd_layer_plan_backward(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
-        const bool nw = take_no_wait(plan, as_stream(stream));
-        if (plan_dense(plan)) {
-            fused_backward(plan->dense_dx, plan->dense_dw, as_stream(stream), nw);
-        } else if (use_masked_dx(plan)) {
-            // dW on the 1-CTA kernel, dX on the 2-CTA kernel: independent
-            // launches, the second never waits for the first
-            launch_gemm(plan->dw, as_stream(stream), nw);
-            launch_gemm(plan->dx_masked, as_stream(stream), true);
-        } else if (use_pairs(plan)) {
-            // dX's row-pair part on the 2-CTA kernel, then dX's remainder and dW
-            // as one 1-CTA launch that fills the SMs the first one leaves
-            launch_dx_pairs(plan, as_stream(stream), nw);
-            fused_backward(plan->dx_rem, plan->dw, as_stream(stream), true);
-        } else {
-            fused_backward(plan->dx, plan->dw, as_stream(stream), nw);
+        plan_backward_impl(plan, as_stream(stream));
+    });
+}
+
+// One CUDA-graph launch per step for host-bound callers (small layers, many
+// layers per step): the step's kernels (mask generation, forward and, with
+// what = 3, the backward — the same launches and PDL edges as the eager
+// calls) are captured once per plan on a private stream; each call patches the
+// seed into the graph's mask node and launches the graph on `stream`. Results
+// equal the eager calls'. Inside the graph the mask generation waits for its
+// predecessor grid (the release-counter overlap needs host tracking), and the
+// next eager generation into the workspace does too.
+int sd_layer_plan_graph_step(sd_layer_plan* plan, uint64_t seed, int32_t what, void* stream) {
+    return guarded([&] {
+        if (!plan) fail(SD_EINVAL, "null plan");
+        if (what != 1 && what != 3) fail(SD_EINVAL, "sd_layer_plan_graph_step: what must be 1 (forward) or 3 (step)");
+        auto& g = plan->graph[what == 3 ? 1 : 0];
+        if (!g.exec) {
+            if (!plan->capture_stream)
+                check_cuda(cudaStreamCreateWithFlags(&plan->capture_stream, cudaStreamNonBlocking),
+                           "cudaStreamCreate(capture)");
+            const cudaStream_t cs = plan->capture_stream;
+            const uint64_t l0 = sd_launch_count();
+            check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+            cudaGraph_t graph = nullptr;
+            try {
+                plan_forward_impl(plan, seed, cs);
+                if (what == 3) plan_backward_impl(plan, cs);
+            } catch (...) {
+                cudaStreamEndCapture(cs, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            check_cuda(cudaStreamEndCapture(cs, &graph), "cudaStreamEndCapture");
+            g.kernels = sd_launch_count() - l0;
+            size_t n = 0;
+            check_cuda(cudaGraphGetNodes(graph, nullptr, &n), "cudaGraphGetNodes");
+            std::vector<cudaGraphNode_t> nodes(n);
+            check_cuda(cudaGraphGetNodes(graph, nodes.data(), &n), "cudaGraphGetNodes");
+            for (cudaGraphNode_t node : nodes) {
+                cudaGraphNodeType type;
+                check_cuda(cudaGraphNodeGetType(node, &type), "cudaGraphNodeGetType");
+                if (type != cudaGraphNodeTypeKernel) continue;
+                cudaKernelNodeParams kp{};
+                check_cuda(cudaGraphKernelNodeGetParams(node, &kp), "cudaGraphKernelNodeGetParams");
+                if (kp.func != mask_plan_kernel_func()) continue;
+                g.mask_node = node;
+                g.mask_params = kp;
+                g.mask_args.assign(static_cast<unsigned char*>(kp.kernelParams[0]),
+                                   static_cast<unsigned char*>(kp.kernelParams[0]) + mask_plan_args_size());
+                break;
+            }
+            if (!g.mask_node) {
+                cudaGraphDestroy(graph);
+                fail(SD_ERUNTIME, "sd_layer_plan_graph_step: no mask node in the captured step");
+            }
+            const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(graph);
+                g.mask_node = nullptr;
+                check_cuda(e, "cudaGraphInstantiate");
+            }
+            g.graph = graph;
         }
+        mask_plan_patch_seed(g.mask_args.data(), mix64_host(seed));
+        void* args[1] = {g.mask_args.data()};
+        cudaKernelNodeParams kp = g.mask_params;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        check_cuda(cudaGraphExecKernelNodeSetParams(g.exec, g.mask_node, &kp), "cudaGraphExecKernelNodeSetParams");
+        check_cuda(cudaGraphLaunch(g.exec, as_stream(stream)), "cudaGraphLaunch");
+        note_launch(g.kernels);
+        // the replay's readers release the workspace counter without host
+        // tracking: the next eager generation waits for the whole grid instead
+        mask_note_untracked(plan->mask.words);
+        plan->fwd_mark = ~0ull;
     });
 }
 

@@ -50,6 +50,10 @@ void note_counter_wait();  // a generation launched in counter mode (sd_dev_mask
 void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix,
                       uint64_t threshold, cudaStream_t s);
 void launch_mask_transpose(const sd_block_mask& in, sd_block_mask& out, cudaStream_t s);
+// graph replays of a plan step: the generation kernel and its seed in a parameter block
+const void* mask_plan_kernel_func();
+size_t mask_plan_args_size();
+void mask_plan_patch_seed(void* args, uint64_t seed_mix);
 void launch_mask_retile(const sd_block_mask& in, int split_m, int split_k, sd_block_mask& out,
                         cudaStream_t s);
 

@@ -561,6 +561,12 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     note_launch();
 }
 
+// CUDA-graph replays of a plan step (sd_capi.cu): the generation kernel's
+// function and its parameter block, whose seed is patched per replay.
+const void* mask_plan_kernel_func() { return reinterpret_cast<const void*>(&mask_plan_kernel); }
+size_t mask_plan_args_size() { return sizeof(PlanArgs); }
+void mask_plan_patch_seed(void* args, uint64_t seed_mix) { static_cast<PlanArgs*>(args)->seed_mix = seed_mix; }
+
 void launch_mask_transpose(const sd_block_mask& in, sd_block_mask& out, cudaStream_t s) {
     const int64_t nwords = (static_cast<int64_t>(in.block_rows) * in.block_cols + 63) / 64;
     const int grid = static_cast<int>((nwords + kThreads - 1) / kThreads);

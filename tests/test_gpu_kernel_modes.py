@@ -426,3 +426,37 @@ def test_row_pair_dx_equals_sdd_bitwise(sd, oracle, M, N, K, p, entry):
     bits = np.unpackbits(np.array(m0, dtype=np.uint64).view(np.uint8), bitorder="little")[: R * C].reshape(R, C)
     blocks = dx0.view(R, 128, C, 128).permute(0, 2, 1, 3).reshape(R, C, -1)
     assert (blocks[torch.from_numpy(bits == 0).cuda()].view(torch.int16) == 0).all()
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1, 0.5, 0.9])
+def test_plan_graph_step_equals_eager(sd, oracle, p):
+    """sd_layer_plan_graph_step: the step captured once into a CUDA graph, the
+    mask seed patched per launch — every replay equals the eager step with the
+    same seed (new seeds give new, oracle-exact masks), and eager steps after
+    graph replays are unaffected."""
+    M, N, K = 2048, 1024, 1536
+    x, w, dy = _dev(oracle, M, K, 1), _dev(oracle, K, N, 2), _dev(oracle, M, N, 3)
+    ref_plan = sd.LayerPlan(x, w, dy, p, dy_ready=True)
+    plan = sd.LayerPlan(x, w, dy, p, dy_ready=True)
+    for seed in (5, 6, 7, 1 << 40):
+        ref_plan.forward(seed)
+        ref_plan.backward()
+        plan.graph_step(seed)
+        torch.cuda.synchronize()
+        for a, b in ((plan.y, ref_plan.y), (plan.dx, ref_plan.dx), (plan.dw, ref_plan.dw)):
+            assert torch.equal(a, b), seed
+        words, _ = oracle.sample_mask(p, 128, 128, seed, M, K)
+        assert np.array_equal(np.array(plan.mask.words(), dtype=np.uint64), words)
+    # forward-only graph, then an eager backward on the user stream
+    plan.graph_step(11, backward=False)
+    plan.backward()
+    ref_plan.forward(11)
+    ref_plan.backward()
+    # and plain eager steps after replays
+    plan.forward(12)
+    plan.backward()
+    ref_plan.forward(12)
+    ref_plan.backward()
+    torch.cuda.synchronize()
+    for a, b in ((plan.y, ref_plan.y), (plan.dx, ref_plan.dx), (plan.dw, ref_plan.dw)):
+        assert torch.equal(a, b)
