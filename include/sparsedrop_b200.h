@@ -271,7 +271,9 @@ SD_API uint64_t sd_launch_count(void);
 /* Scheduler tuning switches for A/B measurements (default 0):
  * 1 no tail halving (half-width units for about the last half wave of narrow launches),
  * 2 no split-K, 4 no heaviest-first row order,
- * 8 backward as two launches instead of one fused launch,
+ * 8 backward always as two launches (default: one fused launch, or two — dX
+ *    then dW, the second not waiting for the first — when the fused launch
+ *    would have at least 48 waves of units, where dW's 128x512 units pay),
  * 16 dense (unmasked) GEMMs on the 1-CTA kernel instead of the 2-CTA
  *    (cta_group::2) kernel,
  * 32 force 128x512 tiles on the 1-CTA kernel, 64 force 128x256 tiles
@@ -294,7 +296,8 @@ SD_API uint64_t sd_launch_count(void);
  *    where the columns allow (default: 256x512 with at least two waves of them),
  * 16384 a plan with 0.3 < p <= 0.7 splits dX by mask-row pairs: the column
  *    blocks both rows of a pair keep run on the 2-CTA kernel, the rest on the
- *    1-CTA sdd kernel (bit-identical; off by default: not faster, measured).
+ *    1-CTA sdd kernel (bit-identical; off by default: not faster, measured),
+ * 32768 a two-launch backward launches dW first, 65536 always one fused launch.
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 

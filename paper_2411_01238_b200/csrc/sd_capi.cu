@@ -814,10 +814,34 @@ bool take_no_wait(sd_layer_plan* plan, cudaStream_t s) {
 // The backward's two GEMMs are independent: run them as ONE persistent launch
 // with a shared heaviest-first queue — dX's coarse full-reduction units first,
 // dW's finer units fill the tail.
+// Fused or two launches? One launch shares its tail between dX and dW but runs
+// both on 128x256 units; two launches let dW run alone on 128x512 units (20
+// instead of 24 KB of operands per 1M MACs) at the cost of one more tail.
+// Measured (tools/ab_steps.py, profiles/r02_split_backward_ab.txt): two
+// launches lose 6% at 4096^3 and 1-2% at 8192^3 (27 waves of fused units),
+// win 3-4% at M = 32768-65536 with K = N = 8192 (69-124 waves), tie at p = 0.3.
+bool split_backward(const sd::GemmCall& dx, const sd::GemmCall& dw) {
+    const int t = sd::tuning();
+    if (t & sd::kTuneNoFusedBackward) return true;
+    if (t & sd::kTuneForceFused) return false;
+    const auto units = [](const sd::GemmArgs& a) {
+        return static_cast<int64_t>(a.n_row_tiles) * ((a.cols_out + sd::kBN - 1) / sd::kBN);
+    };
+    return units(dx.args) + units(dw.args) >= 48LL * sd::num_sms();
+}
+
 void fused_backward(const sd::GemmCall& dx, const sd::GemmCall& dw, cudaStream_t s, bool no_wait) {
-    if (sd::tuning() & sd::kTuneNoFusedBackward) {
-        sd::launch_gemm(dw, s, no_wait);
-        sd::launch_gemm(dx, s);
+    if (split_backward(dx, dw)) {
+        // two launches; the second reads nothing the first writes, so it never
+        // waits for it (its CTAs take the SMs the first one's tail frees).
+        // dX's coarse full-reduction units first, dW's finer ones fill the tail
+        if (sd::tuning() & sd::kTuneSplitDwFirst) {
+            sd::launch_gemm(dw, s, no_wait);
+            sd::launch_gemm(dx, s, true);
+        } else {
+            sd::launch_gemm(dx, s, no_wait);
+            sd::launch_gemm(dw, s, true);
+        }
         return;
     }
     const sd::GemmCall* calls[2] = {&dx, &dw};

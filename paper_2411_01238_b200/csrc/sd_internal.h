@@ -137,7 +137,7 @@ enum TuneFlags : int {
     kTuneNoTailHalving = 1,
     kTuneNoSplitK = 2,
     kTuneNoRowOrder = 4,
-    kTuneNoFusedBackward = 8,
+    kTuneNoFusedBackward = 8,   // the backward is always two launches
     kTuneNoGemm2 = 16,  // dense problems on the 1-CTA kernel instead of the 2-CTA one
     kTuneWide = 32,     // force 128 x 512 units on the 1-CTA kernel
     kTuneNarrow = 64,   // force 128 x 256 units on the 1-CTA kernel
@@ -145,6 +145,9 @@ enum TuneFlags : int {
     kTuneNoMaskOverlap = 256,    // mask generation waits for the whole preceding grid
     kTuneNoGeluTable = 512,      // GELU' evaluated per element instead of from the shared-memory table
     kTuneNoMaskedDense = 1024,   // low-p dX stays on the sdd kernel instead of the masked 2-CTA dense GEMM
+    kTuneSplitDwFirst = 32768,   // a two-launch backward launches dW before dX (default: dX first)
+    kTuneForceFused = 65536,     // the backward is always one fused launch (default: two launches when the
+                                 // fused launch would have >= 48 waves of units)
     kTunePairs = 16384,          // mid-p plans split dX by mask-row pairs (2-CTA + 1-CTA remainder); off
                                  // by default: bit-identical but not faster (profiles/r02_row_pairs_ab.txt)
     kTuneGemm2Narrow = 4096,     // 2-CTA kernel: always 256 x 256 pair tiles

@@ -17,16 +17,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_01238_b200 as sd  # noqa: E402
 
 lib = sd.load_library()
-S = int(sys.argv[1])
+S = sys.argv[1]  # SIZE or M,N,K
+M_, N_, K_ = (int(v) for v in S.split(",")) if "," in S else (int(S),) * 3
 P = float(sys.argv[2])
 variants = [int(v) for v in sys.argv[3].split(",")]
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 10
 K = 20
 plans = []
 for i in range(3):
-    x = torch.randn(S, S, device="cuda").to(torch.bfloat16)
-    w = torch.randn(S, S, device="cuda").to(torch.bfloat16)
-    dy = torch.randn(S, S, device="cuda").to(torch.bfloat16)
+    x = torch.randn(M_, K_, device="cuda").to(torch.bfloat16)
+    w = torch.randn(K_, N_, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(M_, N_, device="cuda").to(torch.bfloat16)
     plans.append(sd.LayerPlan(x, w, dy, P, dy_ready=True))
 
 
