@@ -54,8 +54,10 @@ def parse_args():
     ap.add_argument("--rotate", type=int, default=3,
                     help="input sets cycled step to step (their combined size exceeds L2, so steps run "
                          "back-to-back without an L2 flush)")
-    ap.add_argument("--dw-parts", type=int, default=2,
-                    help="N>1: dW computed in this many row slabs, each all-reduced while the next slab and dX run")
+    ap.add_argument("--dw-parts", type=int, default=None,
+                    help="N>1: dW computed in this many row slabs, each all-reduced while the next slab and dX run "
+                         "(default: 1 for configs[4] — one all-reduce, hidden behind dX; slabbing costs ~4%% of "
+                         "compute there, profiles/r02_split_backward_ab.txt — and 2 for the weak-scaled configs[1])")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (CI check of the data-parallel path)")
     ap.add_argument("--config", choices=["cfg2", "cfg5"], default=None,
@@ -258,6 +260,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.config is None:
         args.config = "cfg2" if world == 1 else "cfg5"
+    if args.dw_parts is None:
+        args.dw_parts = 1 if args.config == "cfg5" else 2
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -742,11 +746,12 @@ def cfg5_config(m_global, kn, p, world, nparts, backend):
         "dtypes": {"x/w/dy/y/dx": "bf16", "dw": "fp32 (all-reduced)", "accumulate": "fp32"},
         "l2": "inputs larger than L2 (each rank's X and dY exceed the 126 MB L2 at every N <= 8)",
         "parallelism": (f"dp{world}: rank g owns global rows [g*M/{world}, (g+1)*M/{world}), shard-local masks "
-                        f"(bit-identical to the global mask rows), W replicated; dW in {nparts} row slabs, each "
-                        + ("sum-all-reduced through the library's NCCL communicator (C-ABI "
-                           "sd_layer_plan_backward_allreduce) on a comm stream while the next slab and dX compute"
-                           if backend == "nccl" else
-                           "all-reduced with torch.distributed (gloo; CI path, several ranks on one GPU)"))
+                        f"(bit-identical to the global mask rows), W replicated; "
+                        + ("dW computed, then ONE sum all-reduce of it on a comm stream while dX computes"
+                           if nparts == 1 else f"dW in {nparts} row slabs, each all-reduced while the next slab and "
+                                               "dX compute")
+                        + (" (the library's NCCL communicator, C-ABI sd_layer_plan_backward_allreduce)"
+                           if backend == "nccl" else " (torch.distributed gloo: CI path, several ranks on one GPU)"))
         if world > 1 else "single GPU (the strong-scaling baseline: the whole M on one B200)",
     }
 

@@ -1124,11 +1124,13 @@ int sd_layer_plan_backward_allreduce(sd_layer_plan* plan, sd_comm* comm, int32_t
             comm_allreduce_sum(comm, g.args.out, static_cast<size_t>(g.args.rows_out) * g.args.cols_out,
                                f32 ? SD_DTYPE_F32 : SD_DTYPE_BF16, cs);
         }
+        // dX reads nothing the dW slabs write: it does not wait for them, and
+        // its CTAs start on the SMs the last slab's tail frees
         if (use_pairs(plan)) {
-            launch_dx_pairs(plan, s, false);
+            launch_dx_pairs(plan, s, true);
             launch_gemm(plan->dx_rem, s, true);
         } else {
-            launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, s);
+            launch_gemm(use_masked_dx(plan) ? plan->dx_masked : plan->dx, s, true);
         }
         if (cs != s) {
             check_cuda(cudaEventRecord(plan->reduced, cs), "cudaEventRecord(all-reduce)");

@@ -56,7 +56,7 @@ def test_bench_cfg5_two_ranks_strong():
     assert d["config"]["workload"].startswith("configs[4]")
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["M_global"] == 8192 and d["config"]["M_per_gpu"] == 4096
-    assert d["gpu_launches"] == 5 * 3  # mask, forward, 2 dW slabs, dX
+    assert d["gpu_launches"] == 4 * 3  # mask, forward, dW (one all-reduce, --dw-parts 1 default), dX
     assert d["comm"]["allreduce_ms"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
