@@ -85,8 +85,13 @@ namespace {
 #ifndef SD_STAGES
 #define SD_STAGES 4
 #endif
+// Stages before a unit's last load at which the next unit is claimed. The
+// claim atomic and the decode's dependent list loads run under the GEMM's own
+// L2 traffic and take several microseconds: with 6 the producer ran dry at unit
+// boundaries; 12-18 are equally good (4096^3 steps -3..-5%, ViT-B fc2 backward
+// -12%, neutral at 8192^3 / cfg4; profiles/r02_claim_lead_ab.txt).
 #ifndef SD_CLAIM_LEAD
-#define SD_CLAIM_LEAD 6  // stages before a unit's last load at which the next unit is claimed
+#define SD_CLAIM_LEAD 14
 #endif
 // wide (128 x 512) tiles: separate A / B rings (a 64-deep stage = one A slot +
 // one or two 256-column B slots)
@@ -583,8 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nst = cur.n_eff == 0 ? 0 : cur.nstages;
                 const int claim_at = nst > kClaimLead ? nst - kClaimLead : 0;
                 if (nst == 0) {
+                    // no loads (zero fill only): the scheduler claimed the next
+                    // unit without waiting for a claim signal
                     ptx::mbar_arrive(sempty_bar + cur_slot);
-                    ptx::mbar_arrive(claim_bar);
                     continue;
                 }
                 const GemmArgs& a = L.p[cur.prob];
@@ -764,11 +770,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0 && !unstaged && !L.release_all) release_workspaces(L);
                 break;
             }
+            // A unit without MMA work (an sdd unit that only zero-fills dropped
+            // blocks, a dsd unit of a fully dropped row) has no loads to wait
+            // for: claim the next unit right away instead of after the
+            // producer's signal (the epilogue zero-fills it in turn).
+            const bool loads = __shfl_sync(0xffffffffu, (t.n_eff > 0 && t.nstages > 0) ? 1 : 0, 0);
             if (lane == 0) {
-                ptx::mbar_wait(claim_bar, cphase);
+                if (loads) ptx::mbar_wait(claim_bar, cphase);
                 u = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
             }
-            cphase ^= 1;
+            if (loads) cphase ^= 1;
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
