@@ -1090,7 +1090,12 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         for (int i = 0; i < n; ++i) total_units += gemm_units(pa[i]);
         GemmArgs& last = pa[order[n - 1]];
         const bool sdd = last.flags & kFlagSDD;
-        if (!wide && !(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units < 12 * sms &&
+        // not for launches of less than one wave: there the halved units only
+        // add epilogues, and a plan's forward and early backward no longer fit
+        // on the SMs side by side (1024^3 layer step at p = 0.1: 24.3 -> 18.1
+        // us, p = 0.5: 18.5 -> 17.6 us; profiles/r02_small_ab.txt)
+        if (!wide && !(g_tuning & kTuneNoTailHalving) && last.splits == 1 && total_units >= sms &&
+            total_units < 12 * sms &&
             (!sdd || last.out_col_blk == 128)) {
             // about half a wave of half-width units: measured -2.5% on the 4096^3
             // fused backward at p = 0.5 and -5% on dX at p = 0.1; two waves' worth

@@ -21,6 +21,7 @@ lib.sd_mask_timeline_read.argtypes = [ctypes.c_void_p]
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 P = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
 BACK_TO_BACK = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # steps per timed burst (bench.py runs them back to back)
+GATE = len(sys.argv) > 4 and sys.argv[4] == "gate"  # spin first: every step is queued before the first runs
 x = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 w = torch.randn(S, S, device="cuda").to(torch.bfloat16)
 dy = torch.randn(S, S, device="cuda").to(torch.bfloat16)
@@ -35,6 +36,8 @@ for it in range(4):
     torch.cuda.synchronize()
     l0 = sd.launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if GATE:
+        torch.cuda._sleep(int(4e6))
     a.record()
     for rep in range(BACK_TO_BACK):
         plan.forward(it * 8 + rep)
