@@ -4,7 +4,7 @@ A caller whose X, W, dY live in (pinned) host memory and who wants Y, dX, dW
 back in host memory every step — the reference-facing contract, where
 `forward`/`backward` take and return host matrices (layer.hpp:85-162). On B200
 the step is PCIe-bound (at 4096^3: 96 MiB in, 128 MiB out vs ~0.25 ms of GPU
-work), so steps are double-buffered across three streams:
+work), so steps rotate over `nslots` buffer sets (default 2; 3 measured no faster) across three streams:
 
     h2d stream : inputs of step i+1      ─┐ overlap
     compute    : mask + fwd + bwd of i    ├─ (PCIe is full duplex)
@@ -22,7 +22,7 @@ from .api import LayerPlan, effective_seed
 class HostLayerPipeline:
     def __init__(self, x_host: torch.Tensor, w_host: torch.Tensor, dy_host: torch.Tensor, p: float,
                  row_block_offset: int = 0, device=None, dw_dtype=torch.float32, seed: int = 0,
-                 layer_index: int = 0):
+                 layer_index: int = 0, nslots: int = 2):
         for name, t in (("x", x_host), ("w", w_host), ("dy", dy_host)):
             if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous bf16 host tensor")
@@ -30,7 +30,9 @@ class HostLayerPipeline:
         self.host_in = (x_host, w_host, dy_host)
         self.seed, self.layer_index = seed, layer_index
         self.slots = []
-        for _ in range(2):
+        if nslots < 2:
+            raise ValueError("nslots must be >= 2")
+        for _ in range(nslots):
             xd = torch.empty_like(x_host, device=dev)
             wd = torch.empty_like(w_host, device=dev)
             dyd = torch.empty_like(dy_host, device=dev)
@@ -52,17 +54,17 @@ class HostLayerPipeline:
     def step(self, i: int, allreduce_dw=None):
         """Enqueue step i (asynchronous). Returns the host output tensors of this
         step (valid once `outputs_ready(i)` / synchronize)."""
-        sl = self.slots[i % 2]
+        sl = self.slots[i % len(self.slots)]
         plan = sl["plan"]
         if sl["used"]:
-            self.s_h2d.wait_event(sl["cmp"])   # step i-2 finished reading this slot's inputs
+            self.s_h2d.wait_event(sl["cmp"])   # step i - nslots finished reading this slot's inputs
         with torch.cuda.stream(self.s_h2d):
             for d, h in zip(sl["in"], self.host_in):
                 d.copy_(h, non_blocking=True)
             sl["h2d"].record(self.s_h2d)
         self.s_cmp.wait_event(sl["h2d"])
         if sl["used"]:
-            self.s_cmp.wait_event(sl["d2h"])   # step i-2's outputs of this slot are on the host
+            self.s_cmp.wait_event(sl["d2h"])   # step i - nslots's outputs of this slot are on the host
         with torch.cuda.stream(self.s_cmp):
             plan.forward(effective_seed(self.seed, i, self.layer_index), stream=self.s_cmp)
             if allreduce_dw is None:

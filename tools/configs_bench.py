@@ -7,7 +7,9 @@ cfg3  ViT-B MLP training step, 65536 tokens, 768 -> 3072 -> 768, SparseDrop
       before each Linear (GELU between), p=0.1/0.5, vs the same step dense
 cfg4  LLM projection M=65536, K=N=8192, p=0.1/0.3/0.5, vs dense
 cfg5  one GPU's row shard of M=524288, K=N=8192 (the G=1 point), p=0.1/0.5
-Timing: CUDA events per step, L2 flushed between steps, 0.3 s sustained
+Timing: CUDA events per step, L2 flushed between steps, each step queued behind
+a short spin kernel (torch.cuda._sleep) so its launches are all enqueued before
+the GPU reaches the first event (device time, not host launch latency), 0.3 s sustained
 pre-roll per configuration (steady power-capped state); dense-equivalent and
 executed TFLOP/s, speed-up vs our dense tcgen05 path on the same buffers.
 Beside each: the reference CPU layer fwd+bwd (oracle/_ref, all host threads,
@@ -52,6 +54,7 @@ def timed(step, steps, preroll_s=0.3):
     tot = 0.0
     for i in range(steps):
         flush_buf.fill_(1.0)
+        torch.cuda._sleep(200000)  # ~100 us: the step's launches are queued before it starts
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         step(100 + i)

@@ -8,6 +8,11 @@ repeats of forward, backward and total with FRESH masks (mask generation inside
 the timed region, SPEC.md:448), L2 flushed between repeats (PAPER.md:174);
 median / p10 / p90 in nanoseconds. effective_gflops = executed FLOPs / median
 (sparsedrop: flops_effective on the realised keep; the others: dense FLOPs).
+Each timed repeat is queued behind a short spin kernel (torch.cuda._sleep, after
+the flush) so the forward and backward launches are all enqueued before the GPU
+reaches the first event: the numbers are device time, not Python/driver launch
+latency (--no-gate restores host-in-the-loop timing; at 1024^3 that measured
+~46 us for every method, i.e. the host).
 Honesty check: sparsedrop's device work counter must equal the
 keep-count prediction for every configuration.
 """
@@ -48,6 +53,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "fig4.csv"))
+    ap.add_argument("--no-gate", action="store_true", help="time with the host enqueue in the loop")
     args = ap.parse_args()
     if args.repeats < 3:
         raise SystemExit("repeats must be >= 3 (SPEC.md:445)")
@@ -74,6 +80,8 @@ def main():
                 tf, tb, tt = [], [], []
                 for i in range(args.repeats):
                     flush_buf.fill_(1.0)
+                    if not args.no_gate:
+                        torch.cuda._sleep(200000)  # ~100 us: covers the host enqueue of the pass
                     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                     e0.record()
                     fwd(1000 + i)
