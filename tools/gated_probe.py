@@ -61,13 +61,22 @@ def main():
         def gstep(i):
             plans[i % 3].graph_step(seed=i)
 
+        ins = [(pl._x, pl._w, pl._dy) for pl in plans] if hasattr(plans[0], "_x") else None
+        tens = [(rnd(S, S), rnd(S, S), rnd(S, S)) for _ in range(3)]
+
+        def cublas(i):
+            x, w, dy = tens[i % 3]
+            x @ w
+            x.t() @ dy
+            dy @ w.t()
+
         out = {"S": S, "p": p}
         t_end = time.time() + 1.0
         while time.time() < t_end:
             for i in range(10):
                 step(i)
                 dense(i)
-        for name, fn in (("sparse", step), ("dense", dense), ("graph", gstep)):
+        for name, fn in (("sparse", step), ("dense", dense), ("graph", gstep), ("cublas", cublas)):
             for gated in (False, True):
                 vals = sorted(measure(fn, gated) for _ in range(5))
                 dev, host = vals[len(vals) // 2]
