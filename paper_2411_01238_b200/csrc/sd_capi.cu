@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -190,40 +191,64 @@ void configure_once_per_device(int key, const std::function<void()>& fn) {
 
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Scheduler-counter slots (sd_internal.h). Eager launches take slots
+// round-robin from a ring owned by their STREAM: launches of one stream overlap
+// at most a few deep (PDL), so a 64-slot ring is never reused while a launch
+// that used a slot still runs, and launches of another stream — however many,
+// however long this one runs — never share its slots. A launch captured into a
+// graph gets a dedicated slot that is never handed out again (it is replayed
+// later, possibly beside eager launches).
 unsigned int* sched_slot(cudaStream_t s) {
-    constexpr int kRing = 256;       // eager launches, round-robin
+    constexpr int kRing = 64;        // eager launches per stream, round-robin
     constexpr int kCaptured = 4096;  // launches captured into graphs, never reused (~10 KB each)
-    static unsigned int* slots[64] = {nullptr};
-    static std::atomic<uint32_t> next{0};
-    static std::atomic<uint32_t> next_captured[64];
+    constexpr size_t kSlotBytes = static_cast<size_t>(kSlotWords) * sizeof(unsigned int);
+    struct Ring {
+        unsigned int* base = nullptr;
+        uint32_t next = 0;
+    };
+    struct DevSlots {
+        unsigned int* captured = nullptr;
+        uint32_t next_captured = 0;
+        std::unordered_map<cudaStream_t, Ring> rings;
+    };
     static std::mutex mu;
+    static DevSlots devs[64];
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     if (dev < 0 || dev >= 64) fail(SD_ERUNTIME, "device index out of range");
-    if (!slots[dev]) {
-        std::lock_guard<std::mutex> lock(mu);
-        if (!slots[dev]) {
-            const size_t bytes = static_cast<size_t>(kRing + kCaptured) * kSlotWords * sizeof(unsigned int);
-            unsigned int* p = nullptr;
-            check_cuda(cudaMalloc(&p, bytes), "cudaMalloc(scheduler slots)");
-            check_cuda(cudaMemset(p, 0, bytes), "cudaMemset(scheduler slots)");
-            check_cuda(cudaDeviceSynchronize(), "scheduler slots init");
-            next_captured[dev].store(0);
-            slots[dev] = p;
-        }
-    }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (s != nullptr && cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
         cudaGetLastError();
         cap = cudaStreamCaptureStatusNone;
     }
+    std::lock_guard<std::mutex> lock(mu);
+    DevSlots& d = devs[dev];
+    if (!d.captured) {
+        // first use on this device (sd_layer_plan_create calls this outside any
+        // capture): the captured-launch slots, zeroed once
+        unsigned int* p = nullptr;
+        check_cuda(cudaMalloc(&p, kCaptured * kSlotBytes), "cudaMalloc(scheduler slots)");
+        check_cuda(cudaMemset(p, 0, kCaptured * kSlotBytes), "cudaMemset(scheduler slots)");
+        check_cuda(cudaDeviceSynchronize(), "scheduler slots init");
+        d.captured = p;
+    }
     if (cap == cudaStreamCaptureStatusActive) {
-        const uint32_t i = next_captured[dev].fetch_add(1, std::memory_order_relaxed);
+        const uint32_t i = d.next_captured++;
         if (i >= static_cast<uint32_t>(kCaptured))
             fail(SD_ERUNTIME, "too many captured GEMM launches (" + std::to_string(kCaptured) + " per device)");
-        return slots[dev] + static_cast<size_t>(kRing + i) * kSlotWords;
+        return d.captured + static_cast<size_t>(i) * kSlotWords;
     }
-    return slots[dev] + static_cast<size_t>(next.fetch_add(1, std::memory_order_relaxed) % kRing) * kSlotWords;
+    Ring& r = d.rings[s];
+    if (!r.base) {
+        // a stream's first eager launch: its ring, zeroed in stream order (the
+        // launch that follows on the same stream sees the zeros)
+        if (d.rings.size() > 1024) fail(SD_ERUNTIME, "scheduler slots: more than 1024 streams on one device");
+        unsigned int* p = nullptr;
+        check_cuda(cudaMalloc(&p, kRing * kSlotBytes), "cudaMalloc(stream scheduler slots)");
+        check_cuda(cudaMemsetAsync(p, 0, kRing * kSlotBytes, s), "cudaMemsetAsync(stream scheduler slots)");
+        r.base = p;
+    }
+    return r.base + static_cast<size_t>(r.next++ % kRing) * kSlotWords;
 }
 
 // ---------------------------------------------------------------- reader tracking

@@ -115,7 +115,7 @@ inline int gemm_units(const GemmArgs& a) {
 // Zeroed {next unit, CTAs done, units decoded, spare} counters for one
 // persistent-kernel launch, followed by kTurnstiles split-K turnstiles (two
 // problems x up to kTurnPerProb/4 output tiles x 4 epilogue row quarters). A
-// ring of slots per device, re-armed by the last CTA of the launch that used
+// ring of slots per stream (sched_slot), re-armed by the last CTA of the launch that used
 // it (turnstiles are reset by each tile's last split). A launch captured into a
 // CUDA graph gets a dedicated slot that is never handed out again (it is
 // replayed later, possibly beside eager launches).

@@ -115,3 +115,42 @@ def test_random_operation_sequences(sd):
     finally:
         for pl in plans:
             lib.sd_layer_plan_destroy(pl["h"])
+
+
+def test_concurrent_streams_keep_their_own_scheduler_slots(sd):
+    """Persistent GEMM launches on several streams at once: each stream's
+    launches take scheduler-counter slots from that stream's own ring
+    (sd_capi.cu sched_slot), so a long launch on one stream never shares its
+    work-stealing counters with launches on another, however many are issued
+    meanwhile. Every output must equal the same GEMM run alone."""
+    torch.manual_seed(11)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    # one long launch (70 units over a 65536-long reduction) and many short ones
+    big_a = torch.randn(70 * 128, 16384, device="cuda").to(torch.bfloat16)
+    big_b = torch.randn(16384, 256, device="cuda").to(torch.bfloat16)
+    big_m = sd.sample_mask(sd.DropoutSpec(0.5, 128, 128, 3), 70 * 128, 16384)
+    small = []
+    for i in range(40):
+        a = torch.randn(256, 512, device="cuda").to(torch.bfloat16)
+        b = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
+        m = sd.sample_mask(sd.DropoutSpec(0.5, 128, 128, 100 + i), 256, 512)
+        small.append((a, b, m))
+    torch.cuda.synchronize()
+    ref_big = sd.dsd_matmul(big_a, big_m, big_b, 2.0)
+    ref_small = [sd.dsd_matmul(a, m, b, 2.0) for a, b, m in small]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        outs = [None] * len(small)
+        with torch.cuda.stream(streams[0]):
+            out_big = sd.dsd_matmul(big_a, big_m, big_b, 2.0, stream=streams[0])
+        for j in range(8):  # > 64 launches per stream ring while the long launch runs
+            for i, (a, b, m) in enumerate(small):
+                st = streams[1 + (i + j) % 2]
+                with torch.cuda.stream(st):
+                    o = sd.dsd_matmul(a, m, b, 2.0, stream=st)
+                if j == 7:
+                    outs[i] = o
+        torch.cuda.synchronize()
+        assert torch.equal(out_big, ref_big), rep
+        for i in range(len(small)):
+            assert torch.equal(outs[i], ref_small[i]), (rep, i)
