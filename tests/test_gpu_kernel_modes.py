@@ -460,3 +460,42 @@ def test_plan_graph_step_equals_eager(sd, oracle, p):
     torch.cuda.synchronize()
     for a, b in ((plan.y, ref_plan.y), (plan.dx, ref_plan.dx), (plan.dw, ref_plan.dw)):
         assert torch.equal(a, b)
+
+
+# Launch sizes around one wave of 128 x 256 units (148 SMs): tail halving is on
+# only from one full wave up (sd_gemm.cu launch_gemms). Fused backward unit
+# counts here (dX 4 per block row + dW 32): 144, 148 and 152.
+WAVE_CASES = [(3584, 1024, 1024), (3712, 1024, 1024), (3840, 1024, 1024)]
+
+
+@pytest.mark.parametrize("M,N,K", WAVE_CASES)
+@pytest.mark.parametrize("p", [0.3, 0.5, 0.9])
+def test_one_wave_boundary_tail_halving_bitwise(sd, oracle, M, N, K, p):
+    """Around the one-wave threshold the default (halving on from one wave),
+    halving forced off (tuning 1) and narrow units give identical bits, and
+    the default matches the oracle on sampled row blocks."""
+    x, w, dy = _dev(oracle, M, K, 31), _dev(oracle, K, N, 32), _dev(oracle, M, N, 33)
+    lib = sd.load_library()
+    outs = {}
+    try:
+        for t in (0, 1, 64):
+            lib.sd_set_tuning(t)
+            outs[t] = _layer_outputs(sd, x, w, dy, p, 77)
+    finally:
+        lib.sd_set_tuning(0)
+    for t in (1, 64):
+        for a, b in zip(outs[0], outs[t]):
+            assert torch.equal(a, b), t
+    y, dx, dw = outs[0]
+    words, _ = oracle.sample_mask(p, 128, 128, 77, M, K)
+    s = sd.dropout_scale(p)
+    xn, wn, dyn = (t.double().cpu().numpy() for t in (x, w, dy))
+    for lo in (0, M - 128):
+        hi = lo + 128
+        ref_y = oracle.dsd_matmul(xn, words, wn, 128, 128, 128, s, row_lo=lo, row_hi=hi)
+        g = y[lo:hi].double().cpu().numpy()
+        assert np.linalg.norm(g - ref_y) <= 4e-3 * max(np.linalg.norm(ref_y), 1e-30)
+    ref_dw = oracle.layer_dw(xn, dyn, words, 128, 128, s, krow_lo=0, krow_hi=128)
+    g = dw[:128].double().cpu().numpy()
+    assert np.linalg.norm(g - ref_dw) <= 1e-5 * max(np.linalg.norm(ref_dw), 1e-30)
+
