@@ -64,6 +64,22 @@ def timed(step, steps, preroll_s=0.3):
     return tot / steps
 
 
+def back_to_back(step, steps=20):
+    """Steps enqueued back to back behind a spin kernel (device time, the
+    regime bench.py measures): ms per step."""
+    for j in range(3):
+        step(j)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(400000)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        step(200 + i)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
 def cpu_reference(M, N, K, p, slab_rows):
     """The reference's layer fwd+bwd (mask generation included) on the first
     `slab_rows` rows, timed with all host threads; ms extrapolated to M rows."""
@@ -102,6 +118,9 @@ def layer_cfg(name, M, N, K, ps, steps, slab_rows=512):
         keep = plan.mask.keep_count() / plan.mask.total_blocks()
         if dense_ms is None:
             dense_ms = timed(lambda i: (plan.dense_forward(), plan.dense_backward()), steps)
+        small = M * N * K <= (1 << 33)
+        b2b = back_to_back(lambda i: (plan.forward(sd.effective_seed(0, i, 0)), plan.backward())) if small else None
+        b2b_dense = back_to_back(lambda i: (plan.dense_forward(), plan.dense_backward())) if small else None
         cpu = cpu_reference(M, N, K, p, slab_rows)
         if cpu:
             cpu["dense_equiv_tflops"] = flops / (cpu["ms_per_step_extrapolated"] * 1e-3) / 1e12
@@ -111,6 +130,9 @@ def layer_cfg(name, M, N, K, ps, steps, slab_rows=512):
                     "dense_equiv_tflops": flops / (ms * 1e-3) / 1e12,
                     "executed_tflops": keep * flops / (ms * 1e-3) / 1e12,
                     "dense_tflops": flops / (dense_ms * 1e-3) / 1e12, "cpu_reference": cpu})
+        if b2b is not None:
+            out[-1].update({"back_to_back_ms_per_step": b2b, "dense_back_to_back_ms_per_step": b2b_dense,
+                            "speedup_vs_dense_back_to_back": b2b_dense / b2b})
         print(json.dumps(out[-1]), flush=True)
         del plan
     del x, w, dy
