@@ -238,14 +238,25 @@ unsigned int* sched_slot(cudaStream_t s) {
             fail(SD_ERUNTIME, "too many captured GEMM launches (" + std::to_string(kCaptured) + " per device)");
         return d.captured + static_cast<size_t>(i) * kSlotWords;
     }
-    Ring& r = d.rings[s];
+    // past kMaxRings distinct streams (640 KB each) the remaining streams share
+    // one overflow ring (the pre-round-2 behaviour: safe unless a launch on one
+    // of them outlives 64 launches on the others)
+    constexpr size_t kMaxRings = 256;
+    const cudaStream_t key =
+        (d.rings.count(s) || d.rings.size() < kMaxRings) ? s : reinterpret_cast<cudaStream_t>(~uintptr_t{0});
+    Ring& r = d.rings[key];
     if (!r.base) {
         // a stream's first eager launch: its ring, zeroed in stream order (the
-        // launch that follows on the same stream sees the zeros)
-        if (d.rings.size() > 1024) fail(SD_ERUNTIME, "scheduler slots: more than 1024 streams on one device");
+        // launch that follows on the same stream sees the zeros; the overflow
+        // ring is zeroed synchronously, it serves several streams)
         unsigned int* p = nullptr;
         check_cuda(cudaMalloc(&p, kRing * kSlotBytes), "cudaMalloc(stream scheduler slots)");
-        check_cuda(cudaMemsetAsync(p, 0, kRing * kSlotBytes, s), "cudaMemsetAsync(stream scheduler slots)");
+        if (key == s) {
+            check_cuda(cudaMemsetAsync(p, 0, kRing * kSlotBytes, s), "cudaMemsetAsync(stream scheduler slots)");
+        } else {
+            check_cuda(cudaMemset(p, 0, kRing * kSlotBytes), "cudaMemset(overflow scheduler slots)");
+            check_cuda(cudaDeviceSynchronize(), "overflow scheduler slots init");
+        }
         r.base = p;
     }
     return r.base + static_cast<size_t>(r.next++ % kRing) * kSlotWords;
