@@ -356,7 +356,8 @@ bool mask_take_release(unsigned int* rel, cudaStream_t s, uint32_t* target) {
 }
 
 static CUtensorMap encode_tmap(const void* base, bool f32, cuuint32_t rank, const cuuint64_t* dims,
-                               const cuuint64_t* strides, const cuuint32_t* box) {
+                               const cuuint64_t* strides, const cuuint32_t* box,
+                               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     std::call_once(g_encode_once, [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -374,7 +375,7 @@ static CUtensorMap encode_tmap(const void* base, bool f32, cuuint32_t rank, cons
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = g_encode(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
                                 const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         std::string shape;
@@ -391,6 +392,14 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
     const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
     const cuuint32_t box[2] = {box_inner, box_outer};
     return encode_tmap(base, f32, 2, dims, strides, box);
+}
+
+CUtensorMap make_tmap_2d_noswizzle(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                                   uint32_t box_outer) {
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    return encode_tmap(base, f32, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld, uint32_t atoms) {
@@ -741,6 +750,8 @@ struct sd_layer_plan {
     std::vector<sd::GemmCall> dw_part;
     int dw_parts = 0;
     const void* x = nullptr;
+    const void* dy = nullptr;
+    const void* w = nullptr;
     int m = 0, n = 0, k = 0;
     // launch count right after this plan's last forward and its stream: the
     // next backward launch may skip the wait for the forward grid if nothing
@@ -1028,6 +1039,8 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dense_dw = prep_dense(x, true, dy, true, dw, dw_dtype, k, n, m);
         tmp.dense_dx = prep_dense(dy, false, w, false, dx, dx_dtype, m, k, n);
         tmp.x = x;
+        tmp.dy = dy;
+        tmp.w = w;
         tmp.m = m, tmp.n = n, tmp.k = k;
         // Masked dense dX: sdd over the kept fraction (1 - p) of the blocks on
         // 1-CTA tiles costs ~1.2-1.4x the 2-CTA kernel's time per MAC
@@ -1179,7 +1192,9 @@ int sd_layer_plan_backward_dx(sd_layer_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) fail(SD_EINVAL, "null plan");
         const bool nw = take_no_wait(plan, as_stream(stream));
-        if (use_pairs(plan)) {
+        if ((sd::tuning() & sd::kTuneDxt) && sd::dxt_supported(plan->dx.args)) {
+            sd::launch_dxt(plan->dx, plan->dy, plan->w, as_stream(stream), nw);
+        } else if (use_pairs(plan)) {
             launch_dx_pairs(plan, as_stream(stream), nw);
             launch_gemm(plan->dx_rem, as_stream(stream), true);
         } else {
@@ -1197,6 +1212,11 @@ static void plan_backward_impl(sd_layer_plan* plan, cudaStream_t s) {
         // launches, the second never waits for the first
         launch_gemm(plan->dw, s, nw);
         launch_gemm(plan->dx_masked, s, true);
+    } else if ((sd::tuning() & sd::kTuneDxt) && sd::dxt_supported(plan->dx.args)) {
+        // dX on the transposed 2-CTA kernel, then dW as its own 1-CTA launch
+        // (never waiting for dX: independent outputs)
+        sd::launch_dxt(plan->dx, plan->dy, plan->w, s, nw);
+        launch_gemm(plan->dw, s, true);
     } else if (use_pairs(plan)) {
         // dX's row-pair part on the 2-CTA kernel, then dX's remainder and dW
         // as one 1-CTA launch that fills the SMs the first one leaves

@@ -152,6 +152,7 @@ enum TuneFlags : int {
                                  // by default: bit-identical but not faster (profiles/r02_row_pairs_ab.txt)
     kTuneGemm2Narrow = 4096,     // 2-CTA kernel: always 256 x 256 pair tiles
     kTuneGemm2Wide = 8192,       // 2-CTA kernel: 256 x 512 pair tiles whenever the columns allow
+    kTuneDxt = 1048576,          // a plan's dX on the transposed 2-CTA kernel (sd_dxt.cu) + dW on its own launch
     kTuneNoOwnBits = 2048,       // masked 2-CTA dX reads keep bits per chunk and releases at exit (the
                                  // > kMaxOwnUnits fallback, forced for tests)
 };
@@ -188,6 +189,14 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
 // bf16 [red][mn] operand (mn contiguous, row pitch ld) as 3D (64, red, mn / 64): box = 128 mn
 // x 64 red in two atom-major 8 KB SW128 atoms; coordinates (0, red0, mn0 / 64).
 CUtensorMap make_tmap_mn_atoms(const void* base, uint64_t mn, uint64_t red, uint64_t ld, uint32_t atoms = 2);
+// 2D map without swizzle (the transposed dX epilogue's 32 x 32 store boxes)
+CUtensorMap make_tmap_2d_noswizzle(const void* base, bool f32, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                                   uint32_t box_outer);
+
+// dX on 2-CTA pairs in the transposed form dX^T = W dY^T (sd_dxt.cu): a
+// layer's bf16 dX over 128 x 128 mask blocks, from its prepared sdd call.
+bool dxt_supported(const GemmArgs& dx);
+void launch_dxt(const GemmCall& dx, const void* dy, const void* w, cudaStream_t s, bool no_wait);
 
 // ---------------------------------------------------------------- NCCL (sd_comm.cu)
 // In-place sum all-reduce of `count` elements (SD_DTYPE_*) on stream s.

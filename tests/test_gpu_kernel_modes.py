@@ -499,3 +499,32 @@ def test_one_wave_boundary_tail_halving_bitwise(sd, oracle, M, N, K, p):
     g = dw[:128].double().cpu().numpy()
     assert np.linalg.norm(g - ref_dw) <= 1e-5 * max(np.linalg.norm(ref_dw), 1e-30)
 
+
+
+DXT = 1048576  # sd_set_tuning bit kTuneDxt: a plan's dX on the transposed 2-CTA kernel (sd_dxt.cu)
+
+
+@pytest.mark.parametrize("M,N,K,p", [(1024, 1024, 1024, 0.5), (2048, 768, 3072, 0.9), (4096, 2048, 4096, 0.5),
+                                     (1536, 1024, 2560, 0.3), (2048, 4096, 1024, 0.7)])
+def test_transposed_2cta_dx_matches_sdd(sd, oracle, M, N, K, p):
+    """dX^T = W dY^T on 2-CTA pairs (two kept blocks of one mask row per MMA):
+    bit-identical to the 1-CTA sdd dX (the same 16-deep MMA chains over n in the
+    same order), dropped blocks exact +0.0, and dW unchanged."""
+    x, w, dy = _dev(oracle, M, K, 41), _dev(oracle, K, N, 42), _dev(oracle, M, N, 43)
+    lib = sd.load_library()
+    ref = _layer_outputs(sd, x, w, dy, p, 91)
+    try:
+        lib.sd_set_tuning(DXT)
+        got = _layer_outputs(sd, x, w, dy, p, 91)
+    finally:
+        lib.sd_set_tuning(0)
+    words, _ = oracle.sample_mask(p, 128, 128, 91, M, K)
+    s = sd.dropout_scale(p)
+    dyn, wn = dy.double().cpu().numpy(), w.double().cpu().numpy()
+    for lo in (0, M - 128):
+        ref_dx = oracle.layer_dx(dyn, wn, words, 128, 128, s, row_lo=lo, row_hi=lo + 128)
+        g = got[1][lo:lo + 128].double().cpu().numpy()
+        assert np.linalg.norm(g - ref_dx) <= 4e-3 * max(np.linalg.norm(ref_dx), 1e-30)
+        assert (got[1][lo:lo + 128].view(torch.int16).cpu().numpy()[ref_dx == 0] == 0).all()
+    assert torch.equal(got[2], ref[2]) and torch.equal(got[0], ref[0])
+    assert torch.equal(got[1], ref[1])
