@@ -67,7 +67,8 @@ typedef struct sd_block_mask {
     int32_t* row_order;   /* R: block rows by kept count, descending (scheduling)  */
     int32_t* col_order;   /* C: block columns by kept count, descending           */
     uint32_t* ticket;     /* internal counters (keep zero; sd_mask_bind reserves 256 B:
-                             [0] completion ticket, [1] reader release count) */
+                             [0] completion ticket, [1] reader release count,
+                             [2] last off-path generation number) */
 } sd_block_mask;
 
 SD_API int sd_abi_version(void);

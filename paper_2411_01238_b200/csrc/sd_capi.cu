@@ -278,6 +278,7 @@ struct ReaderEntry {
     uint32_t pending;
     cudaStream_t stream;
     bool mixed;
+    uint32_t last_gen;  // the last off-path generation number published into the workspace (0: none)
 };
 std::mutex g_reader_mu;
 std::vector<ReaderEntry> g_readers;
@@ -301,7 +302,7 @@ void mask_register_workspace(void* ws, size_t bytes, unsigned int* rel) {
         }
     }
     if (g_readers.size() >= 4096) g_readers.erase(g_readers.begin());  // untracked from now on: safe
-    g_readers.push_back({b, e, rel, 0u, nullptr, false});
+    g_readers.push_back({b, e, rel, 0u, nullptr, false, 0u});
 }
 
 // Exact match on the counter address: only a struct filled by sd_mask_bind
@@ -331,6 +332,17 @@ void mask_note_untracked(const void* p) {
     if (!p) return;
     std::lock_guard<std::mutex> lock(g_reader_mu);
     if (ReaderEntry* e = find_reader_entry(reinterpret_cast<uintptr_t>(p))) e->mixed = true;
+}
+
+uint32_t mask_swap_last_gen(unsigned int* rel, uint32_t gen) {
+    std::lock_guard<std::mutex> lock(g_reader_mu);
+    for (auto& e : g_readers) {
+        if (e.rel != rel) continue;
+        const uint32_t prev = e.last_gen;
+        e.last_gen = gen;
+        return prev;
+    }
+    return 0;
 }
 
 std::atomic<uint64_t> g_counter_waits{0};
@@ -695,6 +707,7 @@ GemmCall prep_layer_dw_part(const GemmCall& full, const void* x, const sd_block_
     g.args.list_idx = full.args.list_idx + static_cast<int64_t>(kb0) * full.args.list_stride;
     g.args.row_order = nullptr;
     g.args.split_rows = full.args.rows_out;  // the full dW's split-K factor (same summation order)
+    g.args.hash_list_off = kb0;              // hash mode: the slab's first mask column
     return g;
 }
 
@@ -752,6 +765,12 @@ struct sd_layer_plan {
     const void* x = nullptr;
     const void* dy = nullptr;
     const void* w = nullptr;
+    // small plans (the whole step fits on the SMs at once, mask grid <= 64 x 64):
+    // the GEMMs evaluate their kept lists from the counter hash (hash mode,
+    // sd_gemm_kernel<false, true>), so the forward runs first and the mask
+    // generation after it, off the critical path (launch_mask_plan off_path)
+    bool small = false;
+    bool hash_active = false;  // the last forward ran in hash mode (its backward must too)
     int m = 0, n = 0, k = 0;
     // launch count right after this plan's last forward and its stream: the
     // next backward launch may skip the wait for the forward grid if nothing
@@ -812,6 +831,7 @@ constexpr double kPairsMaxP = 0.7;  // above: too few common kept blocks per row
 // and -5% at p = 0.3. So p <= 0.2, or p <= 0.3 with at least four waves of
 // 256x256 pair tiles.
 bool use_masked_dx(const sd_layer_plan* plan) {
+    if (plan->hash_active) return false;  // the masked dense dX reads the mask words
     if (!plan->dx_masked_ok || (sd::tuning() & sd::kTuneNoMaskedDense) || !sd::gemm2_routed(plan->dx_masked.args))
         return false;
     const int64_t tiles = static_cast<int64_t>(plan->dx_masked.args.rows_out / 256) * (plan->dx_masked.args.cols_out / 256);
@@ -819,7 +839,7 @@ bool use_masked_dx(const sd_layer_plan* plan) {
 }
 
 bool use_pairs(const sd_layer_plan* plan) {
-    return plan->pairs_ok && (sd::tuning() & sd::kTunePairs) && plan->p > 0.0 && plan->p <= kPairsMaxP &&
+    return !plan->hash_active && plan->pairs_ok && (sd::tuning() & sd::kTunePairs) && plan->p > 0.0 && plan->p <= kPairsMaxP &&
            !use_masked_dx(plan);
 }
 
@@ -1042,6 +1062,16 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
         tmp.dy = dy;
         tmp.w = w;
         tmp.m = m, tmp.n = n, tmp.k = k;
+        {
+            // small: every 128 x 256 unit of the forward, dX and dW runs at once
+            // (< one wave together) and every kept list fits the 64-entry hash
+            // decode; then the mask generation is better off the critical path
+            const auto units = [](const GemmArgs& a) {
+                return static_cast<int64_t>(a.n_row_tiles) * ((a.cols_out + kBN - 1) / kBN);
+            };
+            tmp.small = p > 0.0 && mask->block_rows <= 64 && mask->block_cols <= 64 &&
+                        units(tmp.fwd.args) + units(tmp.dx.args) + units(tmp.dw.args) <= num_sms();
+        }
         // Masked dense dX: sdd over the kept fraction (1 - p) of the blocks on
         // 1-CTA tiles costs ~1.2-1.4x the 2-CTA kernel's time per MAC
         // (profiles/r01_masked_dx_ab.txt), so below p = kMaskedDenseMaxP the
@@ -1104,9 +1134,49 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
 // (all-kept) mask is still generated: the caller's BlockMask stays valid.
 static bool plan_dense(const sd_layer_plan* plan) { return plan->p == 0.0 && !(tuning() & kTuneNarrow); }
 
-static void plan_forward_impl(sd_layer_plan* plan, uint64_t seed, cudaStream_t s) {
-    launch_mask_plan(plan->mask, false, mix64_host(seed), plan->threshold, s);
-    launch_gemm(plan_dense(plan) ? plan->dense_fwd : plan->fwd, s);
+// Hash mode of a small plan's GEMMs (GemmArgs::hash_mode): set on the forward,
+// dX and dW calls (and the dW slabs) for this forward's seed, or cleared.
+static void set_hash(sd::GemmArgs& a, int mode, int len, uint64_t seed_mix, const sd_layer_plan* plan) {
+    a.hash_mode = mode;
+    a.hash_len = len;
+    a.hash_row_off = plan->mask.row_block_offset;
+    a.hash_seed_mix = seed_mix;
+    a.hash_threshold = plan->threshold;
+}
+
+static void plan_set_hash(sd_layer_plan* plan, uint64_t seed_mix, bool on) {
+    const int R = plan->mask.block_rows, C = plan->mask.block_cols;
+    set_hash(plan->fwd.args, on ? 1 : 0, C, seed_mix, plan);
+    set_hash(plan->dx.args, on ? 1 : 0, C, seed_mix, plan);
+    set_hash(plan->dw.args, on ? 2 : 0, R, seed_mix, plan);
+    for (auto& g : plan->dw_part) set_hash(g.args, on ? 2 : 0, R, seed_mix, plan);
+}
+
+static bool stream_capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return st != cudaStreamCaptureStatusNone;
+}
+
+static void plan_forward_impl(sd_layer_plan* plan, uint64_t seed, cudaStream_t s, bool allow_small = true) {
+    const uint64_t sm = mix64_host(seed);
+    const bool dense = plan_dense(plan);
+    const bool small = plan->small && allow_small && !dense && !(sd::tuning() & sd::kTuneNoSmallHash) &&
+                       !stream_capturing(s);
+    plan_set_hash(plan, sm, small);
+    plan->hash_active = small;
+    if (small) {
+        // the forward needs nothing from the mask generation: it goes first, the
+        // generation (for the plan's mask outputs and list readers) after it
+        launch_gemm(plan->fwd, s);
+        launch_mask_plan(plan->mask, false, sm, plan->threshold, s, true);
+    } else {
+        launch_mask_plan(plan->mask, false, sm, plan->threshold, s);
+        launch_gemm(dense ? plan->dense_fwd : plan->fwd, s);
+    }
     plan->fwd_mark = sd_launch_count();
     plan->fwd_stream = s;
 }
@@ -1256,7 +1326,7 @@ int sd_layer_plan_graph_step(sd_layer_plan* plan, uint64_t seed, int32_t what, v
             check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
             cudaGraph_t graph = nullptr;
             try {
-                plan_forward_impl(plan, seed, cs);
+                plan_forward_impl(plan, seed, cs, false);
                 if (what == 3) plan_backward_impl(plan, cs);
             } catch (...) {
                 cudaStreamEndCapture(cs, &graph);

@@ -306,6 +306,120 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& a, int prob, int u) 
     return t;
 }
 
+// ---- hash mode (small plans): decode without the mask workspace ----------
+__device__ __forceinline__ uint64_t mix64_d(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Kept bits of list `idx` (a mask row for hash mode 1, a mask column for 2) over
+// its hash_len <= 64 entries, from the counter hash (block_mask.cpp:70; the
+// mask kernel's keep_bit). Whole scheduler warp; every lane gets the set.
+__device__ __forceinline__ uint64_t hash_list_bits(const GemmArgs& a, int idx, uint32_t lane) {
+    const int li = idx + a.hash_list_off;
+    bool k0 = false, k1 = false;
+    if (a.hash_mode == 1) {
+        const uint64_t hr = mix64_d(a.hash_seed_mix ^ static_cast<uint64_t>(li + a.hash_row_off));
+        if (static_cast<int>(lane) < a.hash_len) k0 = (mix64_d(hr ^ lane) >> 11) >= a.hash_threshold;
+        if (static_cast<int>(lane) + 32 < a.hash_len) k1 = (mix64_d(hr ^ (lane + 32)) >> 11) >= a.hash_threshold;
+    } else {
+        const uint64_t c = static_cast<uint64_t>(li);
+        if (static_cast<int>(lane) < a.hash_len)
+            k0 = (mix64_d(mix64_d(a.hash_seed_mix ^ static_cast<uint64_t>(lane + a.hash_row_off)) ^ c) >> 11) >=
+                 a.hash_threshold;
+        if (static_cast<int>(lane) + 32 < a.hash_len)
+            k1 = (mix64_d(mix64_d(a.hash_seed_mix ^ static_cast<uint64_t>(lane + 32 + a.hash_row_off)) ^ c) >> 11) >=
+                 a.hash_threshold;
+    }
+    return static_cast<uint64_t>(__ballot_sync(0xffffffffu, k0)) |
+           (static_cast<uint64_t>(__ballot_sync(0xffffffffu, k1)) << 32);
+}
+
+// Position of the (n+1)-th set bit of v (n < popcount(v)).
+__device__ __forceinline__ int nth_set_bit64(uint64_t v, int n) {
+    const uint32_t lo = static_cast<uint32_t>(v), hi = static_cast<uint32_t>(v >> 32);
+    const int cl = __popc(lo);
+    return n < cl ? static_cast<int>(__fns(lo, 0, n + 1)) : 32 + static_cast<int>(__fns(hi, 0, n - cl + 1));
+}
+
+// decode_unit's coordinates (no list reads; the tile-row order is not used)
+template <bool WIDE>
+__device__ __forceinline__ Unit decode_coords_h(const GemmArgs& a, int prob, int u, int& cu_out) {
+    Unit t;
+    t.prob = prob;
+    const int T = a.tail_rows;
+    const int head_rows = a.n_row_tiles - T;
+    const int head_units = head_rows * a.n_col_units;
+    const int base_units = head_units + T * 2 * a.n_col_units;
+    const int split = u / base_units;
+    u -= split * base_units;
+    t.split = split;
+    t.tile = u;
+    int i, cu;
+    bool half = false;
+    if (u < head_units) {
+        const int g = u / (kGroupRows * a.n_col_units);
+        const int rem_u = u - g * kGroupRows * a.n_col_units;
+        const int rows_in_group = min(kGroupRows, head_rows - g * kGroupRows);
+        cu = rem_u / rows_in_group;
+        i = g * kGroupRows + (rem_u - cu * rows_in_group);
+    } else {
+        u -= head_units;
+        cu = u / T;
+        i = head_rows + (u - cu * T);
+        half = true;
+    }
+    t.row0 = i * kBM;
+    t.list_row = t.row0 / a.out_row_blk;
+    t.nslots = 0;
+    t.nzero = 0;
+    t.first_entry = 0;
+    t.width = half ? KCfg<WIDE>::kWidth / 2 : KCfg<WIDE>::kWidth;
+    cu_out = cu;
+    return t;
+}
+
+// decode_unit's list-dependent fields, from the unit's kept bits
+template <bool WIDE>
+__device__ __forceinline__ void decode_finish_h(const GemmArgs& a, Unit& t, int cu, uint64_t hbits) {
+    const int width = t.width;
+    const int cnt = __popcll(hbits);
+    if (!(a.flags & kFlagSDD)) {
+        t.n0 = cu * width;
+        const int rem = a.cols_out - t.n0;
+        t.n_eff = rem < width ? (rem > 0 ? rem : 0) : width;
+        const int lo = static_cast<int>((static_cast<int64_t>(cnt) * t.split) / a.splits);
+        const int hi = static_cast<int>((static_cast<int64_t>(cnt) * (t.split + 1)) / a.splits);
+        t.first_entry = lo;
+        t.nstages = (hi - lo) * (a.red_blk / kBK);
+        if (hi == lo) t.n_eff = 0;
+    } else {
+        // kept blocks ascending; dropped blocks ascending (each unit of the row
+        // zero-fills its own share, every dropped block exactly once)
+        const int per_unit = width / a.out_col_blk;
+        const uint64_t all = a.mask_cols == 64 ? ~0ull : ((1ull << a.mask_cols) - 1);
+        const int ndrop = a.mask_cols - cnt;
+        t.n0 = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j >= per_unit) break;
+            const int li = cu * per_unit + j;
+            if (li < cnt) {
+                t.slot_blk[j] = nth_set_bit64(hbits, li);
+                t.nslots = j + 1;
+            }
+            if (li < ndrop) {
+                t.zero_blk[j] = nth_set_bit64(~hbits & all, li);
+                t.nzero = j + 1;
+            }
+        }
+        t.n_eff = t.nslots * a.out_col_blk;
+        t.nstages = a.red / kBK;
+    }
+}
+
 // This CTA is done reading the mask workspaces of the launch (release counters).
 __device__ __forceinline__ void release_workspaces(const LaunchArgs& L) {
     for (int r = 0; r < 2; ++r) {
@@ -486,7 +600,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& a, const CUtensorM
     }
 }
 
-template <bool WIDE>
+template <bool WIDE, bool HASH>
 __global__ void __launch_bounds__(kThreads, 1)
     sd_gemm_kernel(const __grid_constant__ TensorMaps tms, const __grid_constant__ LaunchArgs L) {
     using C = KCfg<WIDE>;
@@ -605,13 +719,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int li0 = sdd ? 0 : cur.first_entry;
                 const int scol0 = cur.slot_blk[0] * a.out_col_blk, scol1 = cur.slot_blk[1] * a.out_col_blk;
                 const int scol2 = cur.slot_blk[2] * a.out_col_blk, scol3 = cur.slot_blk[3] * a.out_col_blk;
-                const int32_t* lst =
-                    (!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
-                                         : nullptr;
                 // kept-block indices: staged in smem by the scheduler (lists up to
-                // kListCap), else read from global one block ahead
+                // kListCap, and every hash-mode list), else read from global one
+                // block ahead
                 const int32_t* slist = sched_list + cur_slot * kListCap;
-                const bool staged = cur.nstages / spb <= kListCap;
+                const int32_t* lst =
+                    HASH ? (sdd ? nullptr : slist)
+                         : ((!sdd && a.list_idx) ? a.list_idx + static_cast<int64_t>(cur.list_row) * a.list_stride + li0
+                                                 : nullptr);
+                const bool staged = HASH || cur.nstages / spb <= kListCap;
                 int kb_next = lst ? (staged ? slist[0] : __ldcg(lst)) : 0;
                 int kb = 0;
                 for (int s = 0, li = 0, sub = 0; s < cur.nstages; ++s) {
@@ -692,6 +808,64 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::mbar_arrive(sempty_bar + cur_slot);  // done with the slot's staged list
             }
+        }
+    } else if (HASH && warp == 3) {
+        // ===================== scheduler (hash mode) =====================
+        // As below, but each unit's kept list comes from the counter hash
+        // (one warp, no loads): the launch reads nothing of the mask workspace.
+        int sslot = 0;
+        uint32_t sphase = 0;
+        uint32_t cphase = 0;
+        int u = blockIdx.x;
+        while (true) {
+            Unit t;
+            int cu = 0;
+            int prob = -1;
+            if (lane == 0) {
+                if (u < num_units) {
+                    prob = (L.nprob > 1 && u >= L.p[1].unit_begin) ? 1 : 0;
+                    t = decode_coords_h<WIDE>(L.p[prob], prob, u - L.p[prob].unit_begin, cu);
+                } else {
+                    t.prob = -1;
+                    t.nslots = 0;
+                }
+            }
+            prob = __shfl_sync(0xffffffffu, prob, 0);
+            uint64_t hbits = 0;
+            if (prob >= 0) hbits = hash_list_bits(L.p[prob], __shfl_sync(0xffffffffu, t.list_row, 0), lane);
+            int nblk = 0, li0 = 0;
+            if (lane == 0 && prob >= 0) {
+                decode_finish_h<WIDE>(L.p[prob], t, cu, hbits);
+                const GemmArgs& a = L.p[prob];
+                if (!(a.flags & kFlagSDD) && t.n_eff > 0) {
+                    nblk = t.nstages / (a.red_blk / kBK);
+                    li0 = t.first_entry;
+                }
+            }
+            nblk = __shfl_sync(0xffffffffu, nblk, 0);
+            li0 = __shfl_sync(0xffffffffu, li0, 0);
+            SD_TWAIT(1, ptx::mbar_wait(sempty_bar + sslot, sphase ^ 1));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = static_cast<int>(lane) + 32 * h;
+                if ((hbits >> j) & 1ull) {
+                    const int pos = __popcll(hbits & ((1ull << j) - 1ull)) - li0;
+                    if (pos >= 0 && pos < nblk) sched_list[sslot * kListCap + pos] = j;
+                }
+            }
+            if (lane == 0) sched_unit[sslot] = t;
+            ptx::mbar_arrive(sfull_bar + sslot);
+            if (++sslot == kSchedDepth) {
+                sslot = 0;
+                sphase ^= 1;
+            }
+            if (prob < 0) break;
+            const bool loads = __shfl_sync(0xffffffffu, (t.n_eff > 0 && t.nstages > 0) ? 1 : 0, 0);
+            if (lane == 0) {
+                if (loads) ptx::mbar_wait(claim_bar, cphase);
+                u = static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(L.sched, 1u));
+            }
+            if (loads) cphase ^= 1;
         }
     } else if (warp == 3) {
         // ===================== scheduler =====================
@@ -1009,12 +1183,15 @@ static bool wide_units(const GemmCall* const* calls, int n) {
 void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_wait) {
     if (n < 1 || n > kMaxProblems) fail(SD_EINVAL, "launch_gemms: 1 or 2 problems per launch");
     configure_once_per_device(0, [] {
-        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         KCfg<false>::kSmem),
                    "cudaFuncSetAttribute(max dynamic smem)");
-        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         KCfg<true>::kSmem),
                    "cudaFuncSetAttribute(max dynamic smem, wide)");
+        check_cuda(cudaFuncSetAttribute(sd_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        KCfg<false>::kSmem),
+                   "cudaFuncSetAttribute(max dynamic smem, hash)");
     });
     // dense problems go to the 2-CTA kernel (half the per-SM operand traffic
     // per MAC: tools/gemm2_check.py, +10-25% over this kernel at 4096-8192)
@@ -1042,7 +1219,11 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     // split 0 stores, the others reduce-add in split order behind a per-tile
     // turnstile, so the result is bit-reproducible run to run.
     // unit width: 128 x 512 (wide) or 128 x 256, one choice per launch
-    const bool wide = wide_units(calls, n);
+    // hash mode (small plans): every problem decodes its lists from the mask's
+    // counter hash; narrow units, no tile-row order, no mask-workspace reads
+    bool hash = true;
+    for (int i = 0; i < n; ++i) hash = hash && calls[i]->args.hash_mode != 0;
+    const bool wide = !hash && wide_units(calls, n);
     const int width = wide ? 2 * kBN : kBN;
     GemmArgs pa[kMaxProblems];
     float cost[kMaxProblems];
@@ -1083,6 +1264,16 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         order[0] = 1;
         order[1] = 0;
     }
+#ifndef SD_SMALL_SDD_HALF
+#define SD_SMALL_SDD_HALF 0
+#endif
+    if (SD_SMALL_SDD_HALF && hash) {
+        // small plans: dX's full-reduction units are the backward's critical
+        // path and the launch leaves SMs idle: one kept block per unit
+        for (int i = 0; i < n; ++i)
+            if ((pa[i].flags & kFlagSDD) && pa[i].out_col_blk == 128 && pa[i].splits == 1)
+                pa[i].tail_rows = pa[i].n_row_tiles;
+    }
     // tail halving on the problem handed out last, when the launch is only a
     // few waves deep: its lightest ~half wave of units become half-width
     {
@@ -1112,7 +1303,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         tms.m[3 * j + 1] = calls[i]->tb;
         tms.m[3 * j + 2] = calls[i]->tout;
         L.p[j] = pa[i];
-        if (g_tuning & kTuneNoRowOrder) L.p[j].row_order = nullptr;
+        if ((g_tuning & kTuneNoRowOrder) || hash) L.p[j].row_order = nullptr;
         L.p[j].unit_begin = total;
         L.p[j].num_units = gemm_units(L.p[j]);
         total += L.p[j].num_units;
@@ -1131,7 +1322,7 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     // bound mask workspaces read by this launch (lists, counts, row orders)
     int nrel = 0;
     bool may_unstage = false;  // a dsd list longer than the scheduler's smem staging
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n && !hash; ++i) {
         unsigned int* r = calls[i]->release;
         if (r && !(nrel > 0 && L.release[0] == r)) L.release[nrel++] = r;
         const GemmArgs& a = L.p[i];
@@ -1148,8 +1339,9 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (wide) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<true>, tms, L), "sd_gemm_kernel<wide> launch");
-    else check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<false>, tms, L), "sd_gemm_kernel launch");
+    if (hash) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<false, true>, tms, L), "sd_gemm_kernel<hash> launch");
+    else if (wide) check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<true, false>, tms, L), "sd_gemm_kernel<wide> launch");
+    else check_cuda(cudaLaunchKernelEx(&cfg, sd_gemm_kernel<false, false>, tms, L), "sd_gemm_kernel launch");
     note_launch();
     for (int r = 0; r < nrel; ++r) mask_note_readers(L.release[r], grid, s);
 }

@@ -47,8 +47,15 @@ bool mask_take_release(unsigned int* rel, cudaStream_t s, uint32_t* target);
 void note_counter_wait();  // a generation launched in counter mode (sd_dev_mask_counter_waits)
 
 // ---------------------------------------------------------------- mask plan
-void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix,
-                      uint64_t threshold, cudaStream_t s);
+// off_path (small plans whose GEMMs hash their lists): every block lets the
+// next launch start at once and waits for the preceding grid before writing;
+// the generation's number is published in ticket word 2 by its last block and
+// the next off-path generation into the workspace waits for it before writing
+// (generations stay ordered by construction). Returns the number (0: none).
+uint32_t launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix,
+                          uint64_t threshold, cudaStream_t s, bool off_path = false);
+// the workspace's last off-path generation number, replaced by `gen`
+uint32_t mask_swap_last_gen(unsigned int* rel, uint32_t gen);
 void launch_mask_transpose(const sd_block_mask& in, sd_block_mask& out, cudaStream_t s);
 // graph replays of a plan step: the generation kernel and its seed in a parameter block
 const void* mask_plan_kernel_func();
@@ -103,6 +110,19 @@ struct GemmArgs {
     float keep_hint;   // nominal kept fraction of the mask (1 - p) when known, else < 0
     int split_rows;    // rows of the full problem that fix the split-K factor (0: rows_out; a dW row
                        // slab passes the full dW's rows so its reduction order equals the full call's)
+    // Hash mode (small plans, sd_gemm_kernel<false, true>): the unit's kept list
+    // comes from the mask's counter hash instead of the list arrays, so the
+    // launch reads nothing of the mask workspace and need not follow the mask
+    // generation: keep(r, c) = (mix64(mix64(seed_mix ^ (r + row_off)) ^ c) >> 11)
+    // >= threshold over hash_len <= 64 entries. 0 = off; 1 = the list of mask
+    // ROW list_row + list_off (forward, dX); 2 = of mask COLUMN list_row +
+    // list_off (dW).
+    int hash_mode;
+    int hash_len;
+    int hash_row_off;   // the mask's row_block_offset (row shards hash their global rows)
+    int hash_list_off;
+    uint64_t hash_seed_mix;
+    uint64_t hash_threshold;
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
@@ -153,6 +173,7 @@ enum TuneFlags : int {
     kTuneGemm2Narrow = 4096,     // 2-CTA kernel: always 256 x 256 pair tiles
     kTuneGemm2Wide = 8192,       // 2-CTA kernel: 256 x 512 pair tiles whenever the columns allow
     kTuneDxt = 1048576,          // a plan's dX on the transposed 2-CTA kernel (sd_dxt.cu) + dW on its own launch
+    kTuneNoSmallHash = 2097152,  // small plans keep the mask generation ahead of list-reading GEMMs
     kTuneNoOwnBits = 2048,       // masked 2-CTA dX reads keep bits per chunk and releases at exit (the
                                  // > kMaxOwnUnits fallback, forced for tests)
 };

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "sd_internal.h"
 
@@ -64,7 +65,19 @@ struct PlanArgs {
     unsigned int* rel;
     uint32_t rel_target;
     int rel_wait;
+    // small plans (hash-mode GEMMs, sd_capi.cu): nothing on the GPU reads this
+    // generation's lists, so every block lets its dependents launch at once
+    // (trigger_early); gen_seq is published in ticket word 2 by the last block
+    // out, and prev_gen (the previous generation into the workspace) is waited
+    // for before the first write, so generations stay ordered by construction
+    int trigger_early;
+    uint32_t gen_seq;
+    uint32_t prev_gen;
 };
+
+__device__ __forceinline__ void publish_generation(const PlanArgs& a) {
+    if (a.gen_seq) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.m.ticket + 2), "r"(a.gen_seq) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long gclock() {
     unsigned long long t;
@@ -78,9 +91,24 @@ __device__ __forceinline__ unsigned long long gclock() {
 // during the tail of the GEMM still finishing on the old mask. Bounded: past
 // 20 ms it falls back to griddepcontrol.wait (always sufficient; the bound only
 // matters if the workspace was re-zeroed behind the library's back).
+__device__ __forceinline__ void wait_previous_generation(const PlanArgs& a) {
+    if (!a.prev_gen) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = gclock();
+        while (true) {
+            unsigned int v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.m.ticket + 2) : "memory");
+            if (v == a.prev_gen || gclock() - t0 > 20000000ull) break;
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void wait_workspace_free(const PlanArgs& a) {
     if (!a.rel_wait) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        wait_previous_generation(a);
         return;
     }
     __shared__ int fallback;
@@ -119,6 +147,7 @@ __device__ __forceinline__ void finish_block(const PlanArgs& a) {
             // out does, so this grid's completion implies its predecessor's
             // under the documented PDL semantics (not only by transitivity)
             if (a.rel_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+            publish_generation(a);
         }
     }
 }
@@ -243,6 +272,7 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     // Compact mode reads the given words, written by earlier work: wait first.
     // Seed mode reads nothing, so every block computes its part first and waits
     // (for the workspace's previous readers) only before its first global write.
+    if (a.trigger_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const bool early = !a.from_words;
     if (!early) {
         wait_workspace_free(a);
@@ -461,11 +491,14 @@ __global__ void __launch_bounds__(kThreads) mask_plan_kernel(const PlanArgs a) {
     }
     order_by_count(a.m.row_cnt, R, C, a.m.row_order, dyn_smem, warp_tot);
     order_by_count(a.m.col_cnt, C, R, a.m.col_order, dyn_smem, warp_tot);
+    __syncthreads();
     if (threadIdx.x == 0) {
         if (a.rel) *a.rel = 0u;  // every block has passed its wait: next round of readers
         *a.m.ticket = 0u;        // re-arm for the next launch on this workspace
+        __threadfence();
         // counter mode: complete only after the preceding grid (see finish_block)
         if (a.rel_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+        publish_generation(a);
     }
 #ifdef SD_TRACE
     if (threadIdx.x == 0) atomicMax(&g_sd_timeline[(a.trace_id & 255) * 4 + 2], gtimer_m());
@@ -507,9 +540,13 @@ __global__ void mask_retile_kernel(const uint64_t* in, int R, int C, int sm, int
 
 }  // namespace
 
-void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix, uint64_t threshold,
-                      cudaStream_t s) {
+uint32_t launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix, uint64_t threshold,
+                          cudaStream_t s, bool off_path) {
+    static std::atomic<uint32_t> g_gen_seq{0x5d000000u};  // process-wide: never repeats per workspace
     PlanArgs a;
+    a.trigger_early = 0;
+    a.gen_seq = 0;
+    a.prev_gen = 0;
     a.trace_id = static_cast<int>(sd_launch_count());
     a.m = m;
     a.from_words = from_words ? 1 : 0;
@@ -521,10 +558,20 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     if (a.rel) {
         uint32_t target = 0;
         const bool ok = mask_take_release(a.rel, s, &target);
-        if (ok && !from_words && !(tuning() & kTuneNoMaskOverlap)) {
+        if (ok && !from_words && !off_path && !(tuning() & kTuneNoMaskOverlap)) {
             a.rel_wait = 1;
             a.rel_target = target;
             note_counter_wait();
+        }
+        if (off_path && !from_words) {
+            // every block waits for the preceding grid (normal mode) but lets the
+            // next launch start right away; generations into this workspace are
+            // chained through ticket word 2
+            a.trigger_early = 1;
+            uint32_t v = g_gen_seq.fetch_add(1) + 1;
+            if (v == 0) v = g_gen_seq.fetch_add(1) + 1;
+            a.gen_seq = v;
+            a.prev_gen = mask_swap_last_gen(a.rel, v);  // the workspace's previous off-path generation
         }
     }
     const int64_t nwords = (static_cast<int64_t>(m.block_rows) * m.block_cols + 63) / 64;
@@ -559,6 +606,7 @@ void launch_mask_plan(const sd_block_mask& m, bool from_words, uint64_t seed_mix
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, mask_plan_kernel, a), "mask_plan_kernel launch");
     note_launch();
+    return a.gen_seq;
 }
 
 // CUDA-graph replays of a plan step (sd_capi.cu): the generation kernel's

@@ -528,3 +528,38 @@ def test_transposed_2cta_dx_matches_sdd(sd, oracle, M, N, K, p):
         assert (got[1][lo:lo + 128].view(torch.int16).cpu().numpy()[ref_dx == 0] == 0).all()
     assert torch.equal(got[2], ref[2]) and torch.equal(got[0], ref[0])
     assert torch.equal(got[1], ref[1])
+
+
+NO_SMALL_HASH = 2097152  # sd_set_tuning bit kTuneNoSmallHash
+
+
+@pytest.mark.parametrize("M,N,K,p", [(1024, 1024, 1024, 0.5), (1024, 1024, 1024, 0.1), (1024, 1024, 1024, 0.9),
+                                     (512, 768, 1536, 0.3), (768, 256, 8192, 0.5), (1024, 512, 1024, 0.95)])
+def test_small_plan_hash_mode_equals_list_mode(sd, oracle, M, N, K, p):
+    """Small plans (the whole step fits on the SMs at once) run their GEMMs in
+    hash mode — kept lists from the counter hash, the forward ahead of the mask
+    generation — and must give the bits of the list-reading path
+    (kTuneNoSmallHash), repeatedly, with the plan's mask equal to the oracle's."""
+    x, w, dy = _dev(oracle, M, K, 51), _dev(oracle, K, N, 52), _dev(oracle, M, N, 53)
+    lib = sd.load_library()
+    plan = sd.LayerPlan(x, w, dy, p, dy_ready=True)
+    outs = []
+    for tune in (0, NO_SMALL_HASH, 0):
+        lib.sd_set_tuning(tune)
+        try:
+            res = []
+            for step in range(3):
+                plan.forward(100 + step)
+                plan.backward()
+                torch.cuda.synchronize()
+                res.append([plan.y.clone(), plan.dx.clone(), plan.dw.clone(),
+                            np.array(plan.mask.words(), dtype=np.uint64)])
+            outs.append(res)
+        finally:
+            lib.sd_set_tuning(0)
+    for step in range(3):
+        words, keep = oracle.sample_mask(p, 128, 128, 100 + step, M, K)
+        for run in outs:
+            assert np.array_equal(run[step][3], words)
+            for a, b in zip(run[step][:3], outs[0][step][:3]):
+                assert torch.equal(a, b)

@@ -153,6 +153,7 @@ def test_untracked_reader_forces_full_wait(sd):
     """A 2-CTA union-mode launch over the workspace's lists does not release:
     the next generation into that workspace must not use the counter."""
     P = _Plans(sd, 1024, 1024, 1024, 0.5, 1)
+    P.lib.sd_set_tuning(2097152)  # kTuneNoSmallHash: this plan's GEMMs read the lists (counter protocol)
     try:
         P.step(0, 5, True)
         torch.cuda.synchronize()
@@ -176,6 +177,37 @@ def test_untracked_reader_forces_full_wait(sd):
         P.step(0, 7, True)  # tracked readers only again: counter mode
         assert lib.sd_dev_mask_counter_waits() == w0 + 1
         torch.cuda.synchronize()
+    finally:
+        P.lib.sd_set_tuning(0)
+        P.close()
+
+
+@pytest.mark.parametrize("M,N,K,p", [(1024, 1024, 1024, 0.5), (512, 768, 1536, 0.1), (1024, 512, 1024, 0.9)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_small_plans_back_to_back_equal_serialized(sd, M, N, K, p, fused):
+    """Small plans (hash-mode GEMMs, the mask generation after the forward and
+    off the critical path, generations into the shared workspace chained through
+    ticket word 2): several plans sharing ONE workspace, steps back to back,
+    bit-identical to the same steps one at a time."""
+    steps = 6
+    P = _Plans(sd, M, N, K, p, steps)
+    try:
+        seeds = [2000 + 31 * i for i in range(steps)]
+        for rep in range(2):
+            for i in range(steps):
+                P.step(i, seeds[i], fused)
+        torch.cuda.synchronize()
+        overlapped = P.snapshot()
+        for o in P.outs:
+            for t in o:
+                t.fill_(float("nan"))
+        for i in range(steps):
+            P.step(i, seeds[i], fused, sync=True)
+            torch.cuda.synchronize()
+        serial = P.snapshot()
+        for i in range(steps):
+            for name, a, b in zip(("y", "dx", "dw"), overlapped[i], serial[i]):
+                assert torch.equal(a, b), f"step {i} {name} differs when small steps overlap"
     finally:
         P.close()
 
