@@ -1150,6 +1150,10 @@ static void plan_set_hash(sd_layer_plan* plan, uint64_t seed_mix, bool on) {
     set_hash(plan->dx.args, on ? 1 : 0, C, seed_mix, plan);
     set_hash(plan->dw.args, on ? 2 : 0, R, seed_mix, plan);
     for (auto& g : plan->dw_part) set_hash(g.args, on ? 2 : 0, R, seed_mix, plan);
+    const auto units = [](const sd::GemmArgs& a) { return a.n_row_tiles * ((a.cols_out + sd::kBN - 1) / sd::kBN); };
+    const int total = units(plan->fwd.args) + units(plan->dx.args) + units(plan->dw.args);
+    plan->fwd.args.hash_plan_units = plan->dx.args.hash_plan_units = plan->dw.args.hash_plan_units = total;
+    for (auto& g : plan->dw_part) g.args.hash_plan_units = total;
 }
 
 static bool stream_capturing(cudaStream_t s) {

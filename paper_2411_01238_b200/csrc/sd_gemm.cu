@@ -1264,15 +1264,19 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         order[0] = 1;
         order[1] = 0;
     }
-#ifndef SD_SMALL_SDD_HALF
-#define SD_SMALL_SDD_HALF 0
-#endif
-    if (SD_SMALL_SDD_HALF && hash) {
+    if (hash) {
         // small plans: dX's full-reduction units are the backward's critical
-        // path and the launch leaves SMs idle: one kept block per unit
-        for (int i = 0; i < n; ++i)
-            if ((pa[i].flags & kFlagSDD) && pa[i].out_col_blk == 128 && pa[i].splits == 1)
+        // path and the step leaves SMs idle, so dX takes one kept block per unit
+        // (1024^3 layer step -8% at p = 0.5, -18% at p = 0.9), and when the whole
+        // step still fits on the SMs with every unit halved, the forward and dW
+        // units are halved too (512^3 -12%, 768^3 -10%; at 1024^3 they would
+        // not fit and the step is 15-28% slower; profiles/r02_small_hash_ab.txt)
+        for (int i = 0; i < n; ++i) {
+            const bool sdd = pa[i].flags & kFlagSDD;
+            const bool all_fit = 2 * pa[i].hash_plan_units <= sms;
+            if (pa[i].splits == 1 && ((sdd && pa[i].out_col_blk == 128) || (!sdd && all_fit)))
                 pa[i].tail_rows = pa[i].n_row_tiles;
+        }
     }
     // tail halving on the problem handed out last, when the launch is only a
     // few waves deep: its lightest ~half wave of units become half-width

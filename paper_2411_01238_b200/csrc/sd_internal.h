@@ -123,6 +123,7 @@ struct GemmArgs {
     int hash_list_off;
     uint64_t hash_seed_mix;
     uint64_t hash_threshold;
+    int hash_plan_units;  // 128 x 256 units of the small plan's whole step (forward + dX + dW)
     int unit_begin;    // filled by launch_gemms: first global unit of this problem
     int num_units;     // filled by launch_gemms
 };
