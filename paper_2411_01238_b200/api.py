@@ -30,9 +30,20 @@ def _lib():
     return _capi.load()
 
 
+_get_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _cur_raw_stream(device: int) -> int:
+    """The current stream of `device` as a raw handle (cheap: no Stream object)."""
+    if _get_raw_stream is not None:
+        return _get_raw_stream(device)
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 def _stream(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return _cur_raw_stream(torch.cuda.current_device())
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -479,30 +490,46 @@ class LayerPlan:
         if dy_ready:
             check(_lib().sd_layer_plan_set_options(self._plan, SD_PLAN_DY_READY))
         self.scale = dropout_scale(p)
+        # the per-step calls, bound once: a small layer's step is ~16 us of
+        # device time, so the Python side of forward()/backward() is kept to
+        # one C call each (no Stream objects, no ctypes wrappers per call)
+        self._dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+        lib = _lib()
+        self._h = self._plan.value
+        self._c_forward = lib.sd_layer_plan_forward
+        self._c_backward = lib.sd_layer_plan_backward
+
+    def _s(self, stream) -> int:
+        return stream.cuda_stream if stream is not None else _cur_raw_stream(self._dev)
 
     def forward(self, seed: int, stream=None):
-        check(_lib().sd_layer_plan_forward(self._plan, seed & MASK64, ctypes.c_void_p(_stream(stream))))
+        rc = self._c_forward(self._h, seed & MASK64,
+                             stream.cuda_stream if stream is not None else _cur_raw_stream(self._dev))
+        if rc:
+            check(rc)
         return self.y
 
     def backward(self, stream=None):
-        check(_lib().sd_layer_plan_backward(self._plan, ctypes.c_void_p(_stream(stream))))
+        rc = self._c_backward(self._h, stream.cuda_stream if stream is not None else _cur_raw_stream(self._dev))
+        if rc:
+            check(rc)
         return self.dx, self.dw
 
     def graph_step(self, seed: int, backward: bool = True, stream=None):
         """forward(seed) [+ backward()] as ONE CUDA-graph launch
         (sd_layer_plan_graph_step): for host-bound callers; same results."""
         check(_lib().sd_layer_plan_graph_step(self._plan, seed & MASK64, 3 if backward else 1,
-                                               ctypes.c_void_p(_stream(stream))))
+                                               self._s(stream)))
         return self.y
 
     def backward_dw(self, stream=None):
-        check(_lib().sd_layer_plan_backward_dw(self._plan, ctypes.c_void_p(_stream(stream))))
+        check(_lib().sd_layer_plan_backward_dw(self._plan, self._s(stream)))
         return self.dw
 
     def backward_dw_part(self, part: int, nparts: int, stream=None):
         """dW rows of mask-column blocks [C*part/nparts, C*(part+1)/nparts): returns
         that row slab of self.dw (bit-identical to the same rows of backward_dw)."""
-        check(_lib().sd_layer_plan_backward_dw_part(self._plan, part, nparts, ctypes.c_void_p(_stream(stream))))
+        check(_lib().sd_layer_plan_backward_dw_part(self._plan, part, nparts, self._s(stream)))
         C, kb = self.mask.block_cols(), self.mask.k_blk()
         return self.dw[(C * part // nparts) * kb:(C * (part + 1) // nparts) * kb]
 
@@ -512,20 +539,20 @@ class LayerPlan:
         summed over the ranks by NCCL on `comm_stream` while the next slab and
         dX compute on `stream`; `stream` then waits for the last all-reduce."""
         cs = ctypes.c_void_p(_stream(comm_stream)) if comm_stream is not None else None
-        check(_lib().sd_layer_plan_backward_allreduce(self._plan, comm._c, nparts, ctypes.c_void_p(_stream(stream)),
+        check(_lib().sd_layer_plan_backward_allreduce(self._plan, comm._c, nparts, self._s(stream),
                                                       cs))
         return self.dx, self.dw
 
     def backward_dx(self, stream=None):
-        check(_lib().sd_layer_plan_backward_dx(self._plan, ctypes.c_void_p(_stream(stream))))
+        check(_lib().sd_layer_plan_backward_dx(self._plan, self._s(stream)))
         return self.dx
 
     def dense_forward(self, stream=None):
-        check(_lib().sd_layer_plan_dense_forward(self._plan, ctypes.c_void_p(_stream(stream))))
+        check(_lib().sd_layer_plan_dense_forward(self._plan, self._s(stream)))
         return self.y
 
     def dense_backward(self, stream=None):
-        check(_lib().sd_layer_plan_dense_backward(self._plan, ctypes.c_void_p(_stream(stream))))
+        check(_lib().sd_layer_plan_dense_backward(self._plan, self._s(stream)))
         return self.dx, self.dw
 
     def __del__(self):
