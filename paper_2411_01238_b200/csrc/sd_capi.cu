@@ -1069,8 +1069,11 @@ int sd_layer_plan_create(sd_layer_plan** out, const void* x, const void* w, cons
             const auto units = [](const GemmArgs& a) {
                 return static_cast<int64_t>(a.n_row_tiles) * ((a.cols_out + kBN - 1) / kBN);
             };
+#ifndef SD_SMALL_ANY
+#define SD_SMALL_ANY 0
+#endif
             tmp.small = p > 0.0 && mask->block_rows <= 64 && mask->block_cols <= 64 &&
-                        units(tmp.fwd.args) + units(tmp.dx.args) + units(tmp.dw.args) <= num_sms();
+                        (SD_SMALL_ANY || units(tmp.fwd.args) + units(tmp.dx.args) + units(tmp.dw.args) <= num_sms());
         }
         // Masked dense dX: sdd over the kept fraction (1 - p) of the blocks on
         // 1-CTA tiles costs ~1.2-1.4x the 2-CTA kernel's time per MAC

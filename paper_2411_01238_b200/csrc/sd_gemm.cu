@@ -1273,8 +1273,8 @@ void launch_gemms(const GemmCall* const* calls, int n, cudaStream_t s, bool no_w
         // not fit and the step is 15-28% slower; profiles/r02_small_hash_ab.txt)
         for (int i = 0; i < n; ++i) {
             const bool sdd = pa[i].flags & kFlagSDD;
-            const bool all_fit = 2 * pa[i].hash_plan_units <= sms;
-            if (pa[i].splits == 1 && ((sdd && pa[i].out_col_blk == 128) || (!sdd && all_fit)))
+            const bool fits = pa[i].hash_plan_units <= sms, all_fit = 2 * pa[i].hash_plan_units <= sms;
+            if (pa[i].splits == 1 && ((sdd && fits && pa[i].out_col_blk == 128) || (!sdd && all_fit)))
                 pa[i].tail_rows = pa[i].n_row_tiles;
         }
     }
