@@ -298,7 +298,14 @@ SD_API uint64_t sd_launch_count(void);
  * 16384 a plan with 0.3 < p <= 0.7 splits dX by mask-row pairs: the column
  *    blocks both rows of a pair keep run on the 2-CTA kernel, the rest on the
  *    1-CTA sdd kernel (bit-identical; off by default: not faster, measured),
- * 32768 a two-launch backward launches dW first, 65536 always one fused launch.
+ * 32768 a two-launch backward launches dW first, 65536 always one fused launch,
+ * 1048576 a plan's dX on the transposed 2-CTA kernel (dX^T = W dY^T, two kept
+ *    blocks of one mask row per pair MMA; bit-identical; off by default: slower,
+ *    measured),
+ * 2097152 small plans keep the list-reading path (default: a plan whose whole
+ *    step fits on the SMs at once, with a mask grid of at most 64 x 64, runs its
+ *    GEMMs from the mask's counter hash and generates the mask after the
+ *    forward, off the critical path; bit-identical).
  * The environment variable SD_TUNING sets the initial value. */
 SD_API int sd_set_tuning(int32_t flags);
 
